@@ -1,0 +1,208 @@
+/*
+ * hsad_gpu.h — C-ABI of the B200-native hsad hot path (sm_100a).
+ *
+ * The reference ("hsad", arXiv 1201.2025) exposes its hot path only as a C++
+ * library API; it has no FFI of its own. These entry points are what a
+ * maintainer binds to replace it (see INTEGRATION.md for the C++ shim and the
+ * ctypes binding). Each entry point names the reference interface it replaces:
+ *
+ *   hsad_daubechies_filters  <- hsad::daubechies_filters   proj/core/include/hsad/wavelet.hpp:24
+ *                                                           (impl proj/core/src/wavelet.cpp:60-74)
+ *   hsad_reduce              <- hsad::reduce_cube           proj/core/include/hsad/wavelet.hpp:55-56
+ *                                                           (impl proj/core/src/wavelet.cpp:148-167)
+ *   hsad_detect              <- hsad::detect / local_rx / dwrx / dwest
+ *                                                           proj/core/include/hsad/detect.hpp:77-92
+ *                                                           (impl proj/core/src/detect.cpp:159-289)
+ *   hsad_detect_multi        <- several hsad::detect calls on one cube that share
+ *                               window statistics (the fused B200 path; same per-detector
+ *                               semantics as hsad_detect)
+ *   hsad_pipeline_host       <- hsad::reduce_cube + hsad::detect on HOST buffers, i.e. the
+ *                               `hsad reduce` + `hsad detect` CLI composition
+ *                               (proj/tools/hsad_main.cpp:112-198) without file I/O
+ *   hsad_mirror_index        <- hsad::mirror_index          proj/core/include/hsad/detect.hpp:68
+ *   hsad_window_validate     <- hsad::WindowConfig::validate proj/core/src/detect.cpp:46-64
+ *
+ * Conventions
+ *  - Cubes are BIP (band fastest), index (row*samples + col)*bands + band, exactly
+ *    hsad::HyperCube (proj/core/include/hsad/cube.hpp:53-58). Element type is fp32
+ *    (elem_bytes = 4, the on-disk type widened by the reference at load,
+ *    cube.cpp:219) or fp64 (elem_bytes = 8, the HyperCube type).
+ *  - Score maps are row-major (row*samples + col), like ScoreMap::scores
+ *    (detect.hpp:52), stored as fp64 (score_bytes = 8, the "fp64 path") or fp32
+ *    (score_bytes = 4, the "fp32 path"; the reference's .raw files are fp32,
+ *    detect.cpp:291-318). All arithmetic is fp64 in both cases.
+ *  - Pointers named d_* are device pointers on the current CUDA device; work is
+ *    enqueued on `stream` (a cudaStream_t, 0 = legacy default stream). Pointers
+ *    named h_* are host pointers.
+ *  - Every call validates its arguments exactly like the reference and returns
+ *    the reference's error category (hsad_status mirrors hsad::errc,
+ *    proj/core/include/hsad/error.hpp:10-32, shifted by one so 0 = success).
+ *    hsad_last_error_message() returns the reference-formatted message of the
+ *    calling thread's last failure: "<Name>: <message>[ at pixel (r, c)]"
+ *    (error.hpp:36-45, detect.cpp:127-130).
+ *  - Per-pixel failures (singular covariance, ...) are reported for the first
+ *    failing pixel in row-major order — the reference's workers=1 semantics
+ *    (parallel.hpp:17-40).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns HSAD_E_CUDA.
+ */
+#ifndef HSAD_GPU_H
+#define HSAD_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSAD_ABI_VERSION 1
+
+typedef enum hsad_status {
+    HSAD_OK = 0,
+    /* hsad::errc + 1 (proj/core/include/hsad/error.hpp:10-32) */
+    HSAD_E_MISSING_KEY = 1,
+    HSAD_E_INVALID_VALUE = 2,
+    HSAD_E_SIZE_MISMATCH = 3,
+    HSAD_E_NON_FINITE_VALUE = 4,
+    HSAD_E_OUT_OF_BOUNDS = 5,
+    HSAD_E_UNSUPPORTED_ORDER = 6,
+    HSAD_E_ODD_LENGTH = 7,
+    HSAD_E_TOO_SHORT = 8,
+    HSAD_E_LENGTH_MISMATCH = 9,
+    HSAD_E_TARGET_TOO_LARGE = 10,
+    HSAD_E_EMPTY_SAMPLE_SET = 11,
+    HSAD_E_TOO_FEW_SAMPLES = 12,
+    HSAD_E_SINGULAR_AFTER_RIDGE = 13,
+    HSAD_E_NOT_SYMMETRIC = 14,
+    HSAD_E_NO_CONVERGENCE = 15,
+    HSAD_E_CONFIG_MISMATCH = 16,
+    HSAD_E_FRACTION_OUT_OF_RANGE = 17,
+    HSAD_E_OUT_OF_BOUNDS_IMPLANT = 18,
+    HSAD_E_DIMENSION_MISMATCH = 19,
+    HSAD_E_DEGENERATE_TRUTH = 20,
+    HSAD_E_IO_FAILURE = 21,
+    /* B200 path only */
+    HSAD_E_CUDA = 64,        /* no device / launch or runtime failure */
+    HSAD_E_UNSUPPORTED = 65  /* outside this build's kernel limits (see hsad_limits) */
+} hsad_status;
+
+typedef enum hsad_algorithm { /* hsad::Algorithm, detect.hpp:13 */
+    HSAD_LRX = 0,
+    HSAD_DWRX = 1,
+    HSAD_DWEST = 2
+} hsad_algorithm;
+
+typedef enum hsad_window_mode { HSAD_WINDOW_SINGLE = 0, HSAD_WINDOW_DUAL = 1 } hsad_window_mode;
+
+/* hsad::WindowConfig (detect.hpp:20-33): Single = one odd window (LRX),
+ * Dual = inner box + outer annulus (DWRX, DWEST). */
+typedef struct hsad_window {
+    int32_t mode;
+    int32_t single_size;
+    int32_t inner_size;
+    int32_t outer_size;
+} hsad_window;
+
+/* One detector request. Mirrors hsad::detect(cube, algo, window, options)
+ * (detect.hpp:91-92) with DetectOptions {ridge, dwest.eigen_fraction}
+ * (detect.hpp:35-45) plus two B200-path extensions:
+ *   guard      LRX only: background = single_size box minus a guard x guard box
+ *              centred on the pixel (1 = the reference: only the centre position
+ *              is excluded, detect.cpp:83-99). Extension, unpinned by the reference.
+ *   d_eigcount DWEST only, nullable: int8 per pixel = number of eigenvectors the
+ *              DWEST loop summed (detect.cpp:258-262). Extension.                */
+typedef struct hsad_detect_request {
+    int32_t algorithm;       /* hsad_algorithm */
+    hsad_window window;
+    int32_t guard;           /* LRX guard box (>= 1, odd); ignored otherwise */
+    double ridge;            /* LRX / DWRX ridge fraction (default 1e-6) */
+    double eigen_fraction;   /* DWEST cutoff fraction in (0, 1] (default 0.1) */
+    void* d_scores;          /* output rows x samples, row-major */
+    int32_t score_bytes;     /* 8 = fp64, 4 = fp32 */
+    int8_t* d_eigcount;      /* DWEST only, nullable */
+} hsad_detect_request;
+
+/* First failing pixel, row-major (global image coordinates). */
+typedef struct hsad_pixel_error {
+    int32_t code;   /* hsad_status, HSAD_OK when no pixel failed */
+    int64_t row;
+    int64_t col;
+} hsad_pixel_error;
+
+/* Kernel limits of this build. */
+typedef struct hsad_limits {
+    int32_t max_detect_bands;   /* bands accepted by hsad_detect* (window-moment kernel) */
+    int32_t max_window;         /* largest single/outer window edge */
+    int32_t max_reduce_bands;   /* bands accepted by hsad_reduce */
+} hsad_limits;
+
+/* ---- library ---------------------------------------------------------------- */
+int32_t hsad_abi_version(void);
+const char* hsad_status_name(int32_t status);      /* errc_name, error.cpp:5-30 */
+const char* hsad_last_error_message(void);          /* thread-local */
+void hsad_get_limits(hsad_limits* out);
+/* 0 when an sm_100-class device is usable; HSAD_E_CUDA otherwise. */
+hsad_status hsad_device_check(void);
+
+/* ---- geometry (host, no device needed) ------------------------------------- */
+int32_t hsad_mirror_index(int32_t i, int32_t n);
+hsad_status hsad_window_validate(const hsad_window* window);
+/* low/high: >= 2*order doubles; *length = 2*order. */
+hsad_status hsad_daubechies_filters(int32_t order, double* low, double* high, int32_t* length);
+
+/* ---- wavelet reduction (reduce_cube) ---------------------------------------- */
+/* d_cube: lines*samples*bands BIP (elem_bytes 4|8); d_out: lines*samples*target_bands
+ * BIP (out_bytes 8|4). Filter: Daubechies `order` (1..10), target_bands a power of
+ * two >= 2 and <= bit_ceil(bands). Errors exactly as wavelet.cpp:122-167. */
+hsad_status hsad_reduce(const void* d_cube, int32_t elem_bytes, int64_t lines, int64_t samples,
+                        int32_t bands, int32_t order, int32_t target_bands, void* d_out,
+                        int32_t out_bytes, void* stream);
+
+/* ---- detectors ---------------------------------------------------------------- */
+/* Whole-image single detector: hsad::detect semantics. Synchronous (the stream is
+ * synchronised to report per-pixel errors); `err` may be NULL. */
+hsad_status hsad_detect(const void* d_cube, int32_t elem_bytes, int64_t lines, int64_t samples,
+                        int32_t bands, const hsad_detect_request* request,
+                        hsad_pixel_error* err, void* stream);
+
+/* Fused multi-detector over a row strip. The image is `lines` x `samples` x
+ * `bands`; the buffer d_cube holds global rows [buf_row0, buf_row0 + buf_rows)
+ * (row strip plus mirror halo; hsad_strip_rows() computes the range) and the
+ * requests' score buffers receive output rows [row_begin, row_end). Window
+ * reflection uses global coordinates, so any row split yields bit-identical maps.
+ * Asynchronous: when d_status (device, 1 x uint64) is non-NULL the first failing
+ * pixel is recorded there as (row*samples+col) << 8 | code (UINT64_MAX = none)
+ * and the call returns without synchronising; decode it with
+ * hsad_decode_status(). With d_status NULL the call synchronises and fills err. */
+hsad_status hsad_detect_multi(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
+                              int64_t row_begin, int64_t row_end,
+                              const hsad_detect_request* requests, int32_t n_requests,
+                              uint64_t* d_status, hsad_pixel_error* err, void* stream);
+
+/* Rows [*buf_row0, *buf_row0 + *buf_rows) that output rows [row_begin, row_end) of a
+ * `lines`-row image read for the given requests (window halo + reflection). */
+hsad_status hsad_strip_rows(int64_t lines, int64_t row_begin, int64_t row_end,
+                            const hsad_detect_request* requests, int32_t n_requests,
+                            int64_t* buf_row0, int64_t* buf_rows);
+/* Row-chunk height the detector grid is anchored to for this image; strip
+ * boundaries that are multiples of it keep per-pixel arithmetic identical. */
+int64_t hsad_row_quantum(int64_t lines, int64_t samples);
+
+hsad_status hsad_decode_status(uint64_t packed, int64_t samples, hsad_pixel_error* err);
+
+/* ---- end to end on host buffers ---------------------------------------------- */
+/* h_cube (fp32 BIP, host; pinned memory recommended) -> H2D -> reduce (order,
+ * target_bands; order 0 = no reduction, detect on the full-band cube) -> all
+ * requests (their d_scores must be HOST pointers here, rows x samples) -> D2H.
+ * Synchronous. Device buffers are cached per thread between calls. */
+hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, int64_t samples, int32_t bands,
+                               int32_t order, int32_t target_bands,
+                               const hsad_detect_request* host_requests, int32_t n_requests,
+                               hsad_pixel_error* err, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* HSAD_GPU_H */

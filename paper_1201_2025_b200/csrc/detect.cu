@@ -1,0 +1,827 @@
+// K2+K3+K4: fused sliding-window statistics and per-pixel solves for Local RX,
+// DWRX and DWEST (hsad::local_rx / dwrx / dwest, proj/core/src/detect.cpp:159-276;
+// statistics proj/core/src/stats.cpp:7-89).
+//
+// The reference gathers every window explicitly (detect.cpp:83-117) and forms a
+// two-pass centred covariance per pixel: O(N L^2) per pixel. Here every window
+// statistic is a *box sum* of per-pixel moments m(p) = (y, upper(y y^T)), with
+// y = x - s shifted by a tile-anchored reference spectrum s (translation
+// invariance of the scores makes the shift exact in real arithmetic and removes
+// the cancellation of S2/N - mu mu^T). Annulus = outer box - inner box, LRX
+// background = box - centre position (or - guard box). Box sums are separable:
+//
+//   * a CTA owns a column strip of NT = TW + 2*rmax virtual columns (thread t owns
+//     virtual column c0 - rmax + t, reflected with mirror_index on *global*
+//     coordinates, detect.cpp:71-76) and streams down a chunk of output rows;
+//   * each thread keeps the vertical window sums of its column for every box in
+//     registers (fp64 running sums: + entering row, - leaving row);
+//   * per output row the vertical sums go through shared memory and each output
+//     thread adds its 2R+1 horizontal neighbours: the full box sums;
+//   * then, still in registers, mean / covariance, ridge, 4x4 Cholesky and the
+//     Mahalanobis form (LRX, DWRX) or a cyclic Jacobi eigensolve, descending
+//     sort, sign rule and the DWEST selection loop.
+//
+// Everything is fp64. The per-pixel summation order depends only on global
+// coordinates and the chunk anchoring, so row strips that start on a multiple
+// of hsad_row_quantum() reproduce the single-GPU map bit for bit.
+#include <cfloat>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hsad_internal.h"
+
+namespace hsad_b200 {
+namespace {
+
+constexpr int kCodeOverflow = 0x80;  // flag: "inverse overflowed" variant of SingularAfterRidge
+
+struct ReqDev {
+    int algo;         // hsad_algorithm
+    int box_a;        // LRX: window box; dual: outer box
+    int box_b;        // LRX: guard box or -1 (centre only); dual: inner box
+    double n_a;       // LRX: background count; dual: inner count
+    double n_b;       // dual: annulus count
+    double ridge;
+    double frac;
+    void* scores;
+    int score_bytes;
+    int8_t* eigcount;
+};
+
+struct DetectParams {
+    const void* cube;
+    int elem_bytes;
+    int64_t lines, samples;
+    int64_t buf_row0, buf_rows;
+    int64_t row_begin, row_end;
+    int64_t chunk;
+    int tw;
+    int rmax;
+    int nbox;
+    int radius[kMaxBoxes];
+    int nreq;
+    ReqDev req[kMaxRequests];
+    unsigned long long* status;
+    int64_t diag_lin;   // >= 0: pixel whose ridge delta is written to diag_out
+    double* diag_out;
+};
+
+template <int L>
+struct Dim {
+    static constexpr int NC = L + L * (L + 1) / 2;  // moment channels
+    static constexpr int NCP = NC | 1;              // odd smem stride: conflict-free LDS.64
+};
+
+__device__ __forceinline__ void report(const DetectParams& P, int64_t row, int64_t col, int code) {
+    const unsigned long long packed =
+        (static_cast<unsigned long long>(row * P.samples + col) << 8) |
+        static_cast<unsigned long long>(code);
+    atomicMin(P.status, packed);
+}
+
+template <int L>
+__device__ __forceinline__ void load_pixel(const DetectParams& P, int64_t vrow, int64_t dcol,
+                                           double (&y)[L]) {
+    const int64_t drow = mirror_index(vrow, P.lines) - P.buf_row0;
+    const int64_t idx = (drow * P.samples + dcol) * L;
+    if (P.elem_bytes == 8) {
+        const double* p = static_cast<const double*>(P.cube) + idx;
+        if constexpr (L % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < L; i += 2) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(p + i));
+                y[i] = v.x;
+                y[i + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < L; ++i) y[i] = __ldg(p + i);
+        }
+    } else {
+        const float* p = static_cast<const float*>(P.cube) + idx;
+#pragma unroll
+        for (int i = 0; i < L; ++i) y[i] = static_cast<double>(__ldg(p + i));
+    }
+}
+
+// m = (y, y_i y_j for i <= j), y already shifted
+template <int L>
+__device__ __forceinline__ void add_moments(double (&acc)[Dim<L>::NC], const double (&y)[L],
+                                            double sign) {
+    int c = L;
+#pragma unroll
+    for (int i = 0; i < L; ++i) acc[i] = fma(sign, y[i], acc[i]);
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) {
+            acc[c] = fma(sign * y[i], y[j], acc[c]);
+            ++c;
+        }
+}
+
+template <int L>
+__device__ __forceinline__ int tri(int i, int j) {  // packed upper index, i <= j
+    return L + i * L - i * (i - 1) / 2 + (j - i);
+}
+
+// mean and covariance (divisor N) from box sums: C = S2/N - mu mu^T
+// (== stats.cpp:13-29 in exact arithmetic on the shifted values)
+template <int L>
+__device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n, double (&mu)[L],
+                                         double (&c)[L][L]) {
+    const double inv = 1.0 / n;
+#pragma unroll
+    for (int i = 0; i < L; ++i) mu[i] = s[i] * inv;
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) {
+            const double v = fma(-mu[i], mu[j], s[tri<L>(i, j)] * inv);
+            c[i][j] = v;
+            c[j][i] = v;
+        }
+}
+
+// regularized_inverse + quadratic form (stats.cpp:31-62, detect.cpp:179-180):
+// delta = ridge tr(C)/L, Cholesky of C + delta I, score = |L^-1 d|^2.
+// Singular rule on the pivots D_j = L_jj^2 (stats.cpp:45-48): a non-positive
+// pivot, or min D <= 1e-14 max D. Returns 0 or an error code.
+template <int L>
+__device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L], double ridge,
+                                         double& score, double& delta) {
+    double tr = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) tr += a[i][i];
+    delta = ridge * tr / static_cast<double>(L);
+#pragma unroll
+    for (int i = 0; i < L; ++i) a[i][i] += delta;
+    double dmax = 0.0, dmin = DBL_MAX;
+    bool ok = true;
+    double z[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        double p = a[j][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) p = fma(-a[j][k], a[j][k], p);
+        ok = ok && (p > 0.0);
+        dmax = fmax(dmax, fabs(p));
+        dmin = fmin(dmin, p);
+        const double ljj = sqrt(fmax(p, 0.0));
+        const double rinv = 1.0 / ljj;
+        a[j][j] = ljj;
+#pragma unroll
+        for (int i = j + 1; i < L; ++i) {
+            double v = a[i][j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v = fma(-a[i][k], a[j][k], v);
+            a[i][j] = v * rinv;
+        }
+        double zj = d[j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) zj = fma(-a[j][k], z[k], zj);
+        z[j] = zj * rinv;
+    }
+    if (!ok || !(dmax > 0.0) || dmin <= dmax * 1e-14) return HSAD_E_SINGULAR_AFTER_RIDGE;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) s = fma(z[j], z[j], s);
+    if (!isfinite(s)) return HSAD_E_SINGULAR_AFTER_RIDGE | kCodeOverflow;
+    score = s;
+    return 0;
+}
+
+// symmetric_eigen (stats.cpp:64-89): cyclic Jacobi with tan-half-angle updates
+// to full fp64 accuracy; descending order (stable), eigenvector sign so that its
+// first largest-|.| component is positive.
+template <int L>
+__device__ __forceinline__ void jacobi_eigen(double (&a)[L][L], double (&v)[L][L], double (&w)[L]) {
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) v[i][j] = i == j ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        double off = 0.0;
+#pragma unroll
+        for (int p = 0; p < L; ++p)
+#pragma unroll
+            for (int q = p + 1; q < L; ++q) off += fabs(a[p][q]);
+        if (off == 0.0) break;
+#pragma unroll
+        for (int p = 0; p < L - 1; ++p)
+#pragma unroll
+            for (int q = p + 1; q < L; ++q) {
+                const double apq = a[p][q];
+                const double g = 100.0 * fabs(apq);
+                if (sweep > 3 && fabs(a[p][p]) + g == fabs(a[p][p]) &&
+                    fabs(a[q][q]) + g == fabs(a[q][q])) {
+                    a[p][q] = 0.0;
+                    a[q][p] = 0.0;
+                } else if (apq != 0.0) {
+                    const double h = a[q][q] - a[p][p];
+                    double t;
+                    if (fabs(h) + g == fabs(h)) {
+                        t = apq / h;
+                    } else {
+                        const double theta = 0.5 * h / apq;
+                        t = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
+                        if (theta < 0.0) t = -t;
+                    }
+                    const double c = 1.0 / sqrt(1.0 + t * t);
+                    const double s = t * c;
+                    const double tau = s / (1.0 + c);
+                    a[p][p] -= t * apq;
+                    a[q][q] += t * apq;
+                    a[p][q] = 0.0;
+                    a[q][p] = 0.0;
+#pragma unroll
+                    for (int k = 0; k < L; ++k) {
+                        if (k == p || k == q) continue;
+                        const double akp = a[k][p], akq = a[k][q];
+                        const double nkp = akp - s * (akq + tau * akp);
+                        const double nkq = akq + s * (akp - tau * akq);
+                        a[k][p] = nkp;
+                        a[p][k] = nkp;
+                        a[k][q] = nkq;
+                        a[q][k] = nkq;
+                    }
+#pragma unroll
+                    for (int k = 0; k < L; ++k) {
+                        const double vkp = v[k][p], vkq = v[k][q];
+                        v[k][p] = vkp - s * (vkq + tau * vkp);
+                        v[k][q] = vkq + s * (vkp - tau * vkq);
+                    }
+                }
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < L; ++i) w[i] = a[i][i];
+    // stable descending bubble sort of (w, columns of v)
+#pragma unroll
+    for (int pass = 0; pass < L - 1; ++pass)
+#pragma unroll
+        for (int i = 0; i < L - 1 - pass; ++i) {
+            if (w[i + 1] > w[i]) {
+                const double tw = w[i];
+                w[i] = w[i + 1];
+                w[i + 1] = tw;
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    const double tv = v[k][i];
+                    v[k][i] = v[k][i + 1];
+                    v[k][i + 1] = tv;
+                }
+            }
+        }
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        double best = -1.0, val = 0.0;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            const double av = fabs(v[k][i]);
+            if (av > best) {
+                best = av;
+                val = v[k][i];
+            }
+        }
+        if (val < 0.0) {
+#pragma unroll
+            for (int k = 0; k < L; ++k) v[k][i] = -v[k][i];
+        }
+    }
+}
+
+__device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s) {
+    if (R.score_bytes == 8) static_cast<double*>(R.scores)[o] = s;
+    else static_cast<float*>(R.scores)[o] = static_cast<float>(s);
+}
+
+template <int L, int NBOX>
+__global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
+    constexpr int NC = Dim<L>::NC;
+    constexpr int NCP = Dim<L>::NCP;
+    extern __shared__ double s_v[];  // [NT][NCP]
+
+    const int t = threadIdx.x;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P.tw;
+    const int64_t vcol = c0 - P.rmax + t;
+    const int64_t dcol = mirror_index(vcol, P.samples);
+    const int64_t ra = P.row_begin + static_cast<int64_t>(blockIdx.y) * P.chunk;
+    const int64_t rb = min(ra + P.chunk, P.row_end);
+    if (ra >= rb) return;
+    const bool out_col = t >= P.rmax && t < P.rmax + P.tw && vcol < P.samples;
+
+    // tile-anchored shift: the spectrum at (ra, c0)
+    double shift[L];
+    {
+        double y[L];
+        load_pixel<L>(P, ra, c0, y);
+#pragma unroll
+        for (int i = 0; i < L; ++i) shift[i] = y[i];
+    }
+    auto shifted = [&](int64_t vrow, double (&y)[L]) {
+        load_pixel<L>(P, vrow, dcol, y);
+#pragma unroll
+        for (int i = 0; i < L; ++i) y[i] -= shift[i];
+    };
+
+    double V[NBOX][NC];
+#pragma unroll
+    for (int k = 0; k < NBOX; ++k) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) V[k][c] = 0.0;
+        const int R = P.radius[k];
+        for (int d = -R; d <= R; ++d) {
+            double y[L];
+            shifted(ra + d, y);
+            add_moments<L>(V[k], y, 1.0);
+        }
+    }
+
+    for (int64_t r = ra; r < rb; ++r) {
+        if (r > ra) {
+#pragma unroll
+            for (int k = 0; k < NBOX; ++k) {
+                const int R = P.radius[k];
+                double yin[L], yout[L];
+                shifted(r + R, yin);
+                shifted(r - 1 - R, yout);
+                add_moments<L>(V[k], yin, 1.0);
+                add_moments<L>(V[k], yout, -1.0);
+            }
+        }
+        double S[NBOX][NC];
+#pragma unroll
+        for (int k = 0; k < NBOX; ++k) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) s_v[t * NCP + c] = V[k][c];
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < NC; ++c) S[k][c] = 0.0;
+            if (out_col) {
+                const int R = P.radius[k];
+                for (int d = -R; d <= R; ++d) {
+                    const double* src = s_v + (t + d) * NCP;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) S[k][c] += src[c];
+                }
+            }
+            __syncthreads();
+        }
+        if (!out_col) continue;
+
+        const int64_t col = vcol;
+        const int64_t o = (r - P.row_begin) * P.samples + col;
+        const int64_t lin = r * P.samples + col;
+        double yc[L];
+        shifted(r, yc);
+
+        for (int q = 0; q < P.nreq; ++q) {
+            const ReqDev& R = P.req[q];
+            if (R.algo == HSAD_LRX) {
+                // detect.cpp:168-188: background = box - centre (or - guard box)
+                double bg[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
+#pragma unroll
+                for (int k = 0; k < NBOX; ++k)
+                    if (k == R.box_a) {
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) bg[c] = S[k][c];
+                    }
+                if (R.box_b < 0) {
+                    add_moments<L>(bg, yc, -1.0);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NBOX; ++k)
+                        if (k == R.box_b) {
+#pragma unroll
+                            for (int c = 0; c < NC; ++c) bg[c] -= S[k][c];
+                        }
+                }
+                double mu[L], cm[L][L], dv[L];
+                mean_cov<L>(bg, R.n_a, mu, cm);
+                double dmax = 0.0;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    dv[i] = yc[i] - mu[i];
+                    dmax = fmax(dmax, fabs(dv[i]));
+                }
+                double score = 0.0;
+                if (dmax > 0.0) {
+                    double delta = 0.0;
+                    const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
+                    if (lin == P.diag_lin) *P.diag_out = delta;
+                    if (code) {
+                        report(P, r, col, code);
+                        score = 0.0;
+                    }
+                }
+                store_score(R, o, fmax(score, 0.0));
+            } else {
+                double sin_[NC], sann[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    sin_[c] = 0.0;
+                    sann[c] = 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < NBOX; ++k) {
+                    if (k == R.box_b) {
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) sin_[c] = S[k][c];
+                    }
+                    if (k == R.box_a) {
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) sann[c] = S[k][c];
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) sann[c] -= sin_[c];
+                double mu_in[L], mu_out[L], c_out[L][L], md[L];
+                double c_in[L][L];
+                mean_cov<L>(sin_, R.n_a, mu_in, c_in);
+                mean_cov<L>(sann, R.n_b, mu_out, c_out);
+                double mmax = 0.0;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    md[i] = mu_in[i] - mu_out[i];
+                    mmax = fmax(mmax, fabs(md[i]));
+                }
+                if (R.algo == HSAD_DWRX) {
+                    // detect.cpp:204-223
+                    double score = 0.0;
+                    if (mmax > 0.0) {
+                        double delta = 0.0;
+                        const int code = chol_quad<L>(c_out, md, R.ridge, score, delta);
+                        if (lin == P.diag_lin) *P.diag_out = delta;
+                        if (code) {
+                            report(P, r, col, code);
+                            score = 0.0;
+                        }
+                    }
+                    store_score(R, o, fabs(score));
+                } else {
+                    // detect.cpp:242-271
+                    double cd[L][L], vec[L][L], w[L];
+#pragma unroll
+                    for (int i = 0; i < L; ++i)
+#pragma unroll
+                        for (int j = 0; j < L; ++j) cd[i][j] = c_in[i][j] - c_out[i][j];
+                    jacobi_eigen<L>(cd, vec, w);
+                    double score = 0.0;
+                    int count = 0;
+                    const double lmax = w[0];
+                    if (lmax > 0.0) {
+                        double proj = 0.0;
+                        bool go = true;
+#pragma unroll
+                        for (int i = 0; i < L; ++i) {
+                            go = go && !(w[i] <= 0.0 || w[i] < R.frac * lmax);
+                            if (go) {
+                                double dot = 0.0;
+#pragma unroll
+                                for (int k = 0; k < L; ++k) dot = fma(vec[k][i], md[k], dot);
+                                proj += dot;
+                                ++count;
+                            }
+                        }
+                        score = fabs(proj);
+                    }
+                    store_score(R, o, score);
+                    if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
+                }
+            }
+        }
+    }
+}
+
+template <int L>
+cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(nt) * Dim<L>::NCP * sizeof(double);
+    switch (P.nbox) {
+#define HSAD_DK(NB)                                                                   \
+    case NB: {                                                                        \
+        auto k = detect_kernel<L, NB>;                                                \
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             static_cast<int>(smem));                 \
+        if (e != cudaSuccess) return e;                                               \
+        k<<<grid, nt, smem, s>>>(P);                                                  \
+        return cudaGetLastError();                                                    \
+    }
+        HSAD_DK(1)
+        HSAD_DK(2)
+        HSAD_DK(3)
+        HSAD_DK(4)
+#undef HSAD_DK
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_detect(int bands, const DetectParams& P, dim3 grid, int nt, cudaStream_t s) {
+    switch (bands) {
+        case 1: return launch_l<1>(P, grid, nt, s);
+        case 2: return launch_l<2>(P, grid, nt, s);
+        case 3: return launch_l<3>(P, grid, nt, s);
+        case 4: return launch_l<4>(P, grid, nt, s);
+        case 5: return launch_l<5>(P, grid, nt, s);
+        case 6: return launch_l<6>(P, grid, nt, s);
+        case 7: return launch_l<7>(P, grid, nt, s);
+        case 8: return launch_l<8>(P, grid, nt, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int device_sms() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+const char* algo_name(int a) {
+    return a == HSAD_LRX ? "local_rx" : a == HSAD_DWRX ? "dwrx" : a == HSAD_DWEST ? "dwest" : "?";
+}
+
+struct Plan {
+    DetectParams P{};
+    int nt = 128;
+    dim3 grid;
+};
+
+// Validate requests (detect.cpp:119-125, 233-234) and resolve the distinct box radii.
+hsad_status plan_requests(const hsad_detect_request* reqs, int n, Plan& plan) {
+    if (n < 1 || n > kMaxRequests)
+        return set_error(HSAD_E_INVALID_VALUE,
+                         "between 1 and " + std::to_string(kMaxRequests) + " requests per call");
+    if (!reqs) return set_error(HSAD_E_INVALID_VALUE, "null request list");
+    DetectParams& P = plan.P;
+    P.nbox = 0;
+    auto box_of = [&](int size) -> int {
+        const int r = size / 2;
+        for (int k = 0; k < P.nbox; ++k)
+            if (P.radius[k] == r) return k;
+        if (P.nbox == kMaxBoxes) return -1;
+        P.radius[P.nbox] = r;
+        return P.nbox++;
+    };
+    P.nreq = n;
+    for (int q = 0; q < n; ++q) {
+        const hsad_detect_request& r = reqs[q];
+        ReqDev& d = P.req[q];
+        hsad_status st = window_validate(r.window);
+        if (st != HSAD_OK) return st;
+        if (r.algorithm == HSAD_LRX) {
+            if (r.window.mode != HSAD_WINDOW_SINGLE)
+                return set_error(HSAD_E_CONFIG_MISMATCH, "local_rx requires a single window");
+            const int w = r.window.single_size;
+            const int g = r.guard <= 0 ? 1 : r.guard;
+            if (g % 2 == 0 || g >= w)
+                return set_error(HSAD_E_INVALID_VALUE,
+                                 "guard window must be odd, >= 1 and < window, got " +
+                                     std::to_string(g));
+            if (!(r.ridge >= 0.0))
+                return set_error(HSAD_E_INVALID_VALUE, "ridge fraction must be nonnegative");
+            d.box_a = box_of(w);
+            d.box_b = g == 1 ? -1 : box_of(g);
+            d.n_a = static_cast<double>(w) * w - static_cast<double>(g) * g;
+            d.n_b = 0.0;
+        } else if (r.algorithm == HSAD_DWRX || r.algorithm == HSAD_DWEST) {
+            if (r.window.mode != HSAD_WINDOW_DUAL)
+                return set_error(HSAD_E_CONFIG_MISMATCH,
+                                 std::string(algo_name(r.algorithm)) + " requires a dual window");
+            if (r.algorithm == HSAD_DWEST && !(r.eigen_fraction > 0.0 && r.eigen_fraction <= 1.0))
+                return set_error(HSAD_E_INVALID_VALUE, "eigen fraction must be in (0, 1]");
+            if (r.algorithm == HSAD_DWRX && !(r.ridge >= 0.0))
+                return set_error(HSAD_E_INVALID_VALUE, "ridge fraction must be nonnegative");
+            d.box_a = box_of(r.window.outer_size);
+            d.box_b = box_of(r.window.inner_size);
+            d.n_a = static_cast<double>(r.window.inner_size) * r.window.inner_size;
+            d.n_b = static_cast<double>(r.window.outer_size) * r.window.outer_size - d.n_a;
+        } else {
+            return set_error(HSAD_E_INVALID_VALUE, "unknown algorithm");
+        }
+        if (d.box_a < 0 || (r.algorithm != HSAD_LRX && d.box_b < 0) ||
+            (r.algorithm == HSAD_LRX && r.guard > 1 && d.box_b < 0))
+            return set_error(HSAD_E_UNSUPPORTED,
+                             "more than " + std::to_string(kMaxBoxes) + " distinct window sizes");
+        d.algo = r.algorithm;
+        d.ridge = r.ridge;
+        d.frac = r.eigen_fraction;
+        d.scores = r.d_scores;
+        d.score_bytes = r.score_bytes;
+        d.eigcount = r.algorithm == HSAD_DWEST ? r.d_eigcount : nullptr;
+        if (r.score_bytes != 4 && r.score_bytes != 8)
+            return set_error(HSAD_E_INVALID_VALUE, "score_bytes must be 4 or 8");
+    }
+    P.rmax = 0;
+    for (int k = 0; k < P.nbox; ++k) P.rmax = P.radius[k] > P.rmax ? P.radius[k] : P.rmax;
+    if (P.rmax > kMaxRadius)
+        return set_error(HSAD_E_UNSUPPORTED, "window edge above " +
+                                                 std::to_string(2 * kMaxRadius + 1) +
+                                                 " is outside this build's kernel limits");
+    return HSAD_OK;
+}
+
+}  // namespace
+
+int64_t row_quantum(int64_t lines, int64_t samples) {
+    // chunk height: large enough to amortise the 2R+1-row warm-up, small enough
+    // that the grid fills the GPU twice (148 SMs); depends on the image only
+    const int sms = 148;
+    const int64_t strips = (samples + 117) / 118;
+    int64_t q = 64;
+    while (q > 8 && strips * ((lines + q - 1) / q) < 2 * sms) q /= 2;
+    return q;
+}
+
+hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
+                              int64_t row_begin, int64_t row_end,
+                              const hsad_detect_request* requests, int32_t n_requests,
+                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s) {
+    if (err) {
+        err->code = HSAD_OK;
+        err->row = err->col = -1;
+    }
+    Plan plan;
+    hsad_status st = plan_requests(requests, n_requests, plan);
+    if (st != HSAD_OK) return st;
+    if (elem_bytes != 4 && elem_bytes != 8)
+        return set_error(HSAD_E_INVALID_VALUE, "elem_bytes must be 4 or 8");
+    if (bands < 1 || bands > kMaxDetectBands)
+        return set_error(HSAD_E_UNSUPPORTED, "hsad_detect supports 1.." +
+                                                 std::to_string(kMaxDetectBands) +
+                                                 " bands (reduce the cube first), got " +
+                                                 std::to_string(bands));
+    if (lines < 0 || samples < 0 || row_begin < 0 || row_end > lines || row_begin > row_end)
+        return set_error(HSAD_E_INVALID_VALUE, "row range outside the image");
+    if (row_begin == row_end || samples == 0) return HSAD_OK;
+    // rows the windows touch must be resident in the buffer
+    int64_t need0 = 0, need_rows = 0;
+    st = hsad_strip_rows(lines, row_begin, row_end, requests, n_requests, &need0, &need_rows);
+    if (st != HSAD_OK) return st;
+    if (need0 < buf_row0 || need0 + need_rows > buf_row0 + buf_rows)
+        return set_error(HSAD_E_OUT_OF_BOUNDS,
+                         "buffer rows [" + std::to_string(buf_row0) + ", " +
+                             std::to_string(buf_row0 + buf_rows) + ") do not cover the window rows [" +
+                             std::to_string(need0) + ", " + std::to_string(need0 + need_rows) + ")");
+    for (int q = 0; q < n_requests; ++q)
+        if (!requests[q].d_scores) return set_error(HSAD_E_INVALID_VALUE, "null score buffer");
+    // DWEST with a 1-pixel inner box: covariance(inner) throws TooFewSamples at the
+    // first pixel (stats.cpp:15-17 via detect.cpp:252-253)
+    for (int q = 0; q < n_requests; ++q)
+        if (requests[q].algorithm == HSAD_DWEST && requests[q].window.inner_size == 1) {
+            if (err) {
+                err->code = HSAD_E_TOO_FEW_SAMPLES;
+                err->row = row_begin;
+                err->col = 0;
+            }
+            // detect.cpp:127-130 rethrows with the inner "<Name>: " kept
+            return set_error(HSAD_E_TOO_FEW_SAMPLES,
+                             "TooFewSamples: covariance needs at least 2 samples, got 1 at pixel (" +
+                                 std::to_string(row_begin) + ", 0)");
+        }
+
+    DetectParams& P = plan.P;
+    P.cube = d_cube;
+    P.elem_bytes = elem_bytes;
+    P.lines = lines;
+    P.samples = samples;
+    P.buf_row0 = buf_row0;
+    P.buf_rows = buf_rows;
+    P.row_begin = row_begin;
+    P.row_end = row_end;
+    P.chunk = row_quantum(lines, samples);
+    plan.nt = 2 * P.rmax + 32 <= 128 ? 128 : 256;
+    P.tw = plan.nt - 2 * P.rmax;
+    P.diag_lin = -1;
+    P.diag_out = nullptr;
+    const int64_t strips = (samples + P.tw - 1) / P.tw;
+    const int64_t chunks = (row_end - row_begin + P.chunk - 1) / P.chunk;
+    if (chunks > 65535) return set_error(HSAD_E_UNSUPPORTED, "image too tall for one launch");
+    plan.grid = dim3(static_cast<unsigned>(strips), static_cast<unsigned>(chunks));
+
+    const bool sync = d_status == nullptr;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(d_status);
+    if (sync) {
+        // the caller-owned d_status accumulates (atomicMin) across calls; the
+        // internal one is reset here
+        HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), 2 * sizeof(double), s));
+        HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
+    }
+    P.status = status;
+    cudaError_t e = launch_detect(bands, P, plan.grid, plan.nt, s);
+    if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
+    if (!sync) return HSAD_OK;
+
+    unsigned long long packed = 0;
+    HSAD_CUDA_TRY(cudaMemcpyAsync(&packed, status, sizeof(packed), cudaMemcpyDeviceToHost, s));
+    HSAD_CUDA_TRY(cudaStreamSynchronize(s));
+    hsad_status result = HSAD_OK;
+    if (packed != ~0ull) {
+        const int code = static_cast<int>(packed & 0x7f);
+        const bool overflow = (packed & kCodeOverflow) != 0;
+        const int64_t lin = static_cast<int64_t>(packed >> 8);
+        const int64_t row = lin / samples, col = lin % samples;
+        std::string msg;
+        if (overflow) {
+            msg = "inverse overflowed";
+        } else {
+            // re-run the failing row to recover that pixel's ridge for the message
+            double delta = 0.0;
+            double* d_diag = reinterpret_cast<double*>(status) + 1;
+            DetectParams D = P;
+            D.row_begin = row;
+            D.row_end = row + 1;
+            D.diag_lin = lin;
+            D.diag_out = d_diag;
+            // the diagnostic pass writes into scratch rows, never over the results
+            char* scratch = nullptr;
+            e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                static_cast<size_t>(samples) * 9 * D.nreq, s);
+            if (e != cudaSuccess) return cuda_fail(e, "hsad detect diagnostics");
+            for (int q = 0; q < D.nreq; ++q) {
+                D.req[q].scores = scratch + static_cast<size_t>(samples) * 9 * q;
+                if (D.req[q].eigcount)
+                    D.req[q].eigcount = reinterpret_cast<int8_t*>(
+                        scratch + static_cast<size_t>(samples) * (9 * q + 8));
+            }
+            e = launch_detect(bands, D, dim3(plan.grid.x, 1), plan.nt, s);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(&delta, d_diag, sizeof(double), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            cudaFreeAsync(scratch, s);
+            if (e != cudaSuccess) return cuda_fail(e, "hsad detect diagnostics");
+            msg = "covariance numerically singular (ridge " + std::to_string(delta) + ")";
+        }
+        result = static_cast<hsad_status>(code);
+        set_error(result, std::string(status_name(code)) + ": " + msg + " at pixel (" +
+                              std::to_string(row) + ", " + std::to_string(col) + ")");
+        if (err) {
+            err->code = code;
+            err->row = row;
+            err->col = col;
+        }
+    }
+    cudaFreeAsync(status, s);
+    return result;
+}
+
+}  // namespace hsad_b200
+
+using namespace hsad_b200;
+
+extern "C" {
+
+int64_t hsad_row_quantum(int64_t lines, int64_t samples) { return row_quantum(lines, samples); }
+
+hsad_status hsad_strip_rows(int64_t lines, int64_t row_begin, int64_t row_end,
+                            const hsad_detect_request* requests, int32_t n_requests,
+                            int64_t* buf_row0, int64_t* buf_rows) {
+    int rmax = 0;
+    for (int q = 0; q < n_requests; ++q) {
+        const hsad_window& w = requests[q].window;
+        const int size = w.mode == HSAD_WINDOW_SINGLE ? w.single_size : w.outer_size;
+        rmax = size / 2 > rmax ? size / 2 : rmax;
+    }
+    if (row_begin >= row_end) {
+        *buf_row0 = row_begin;
+        *buf_rows = 0;
+        return HSAD_OK;
+    }
+    int64_t lo = INT64_MAX, hi = -1;
+    if (row_begin - rmax >= 0 && row_end + rmax <= lines) {
+        lo = row_begin - rmax;
+        hi = row_end + rmax - 1;
+    } else {
+        for (int64_t r = row_begin - rmax; r < row_end + rmax; ++r) {
+            const int64_t m = mirror_index(r, lines);
+            lo = m < lo ? m : lo;
+            hi = m > hi ? m : hi;
+        }
+    }
+    *buf_row0 = lo;
+    *buf_rows = hi - lo + 1;
+    return HSAD_OK;
+}
+
+hsad_status hsad_detect_multi(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
+                              int64_t row_begin, int64_t row_end,
+                              const hsad_detect_request* requests, int32_t n_requests,
+                              uint64_t* d_status, hsad_pixel_error* err, void* stream) {
+    return detect_multi_impl(d_cube, elem_bytes, lines, samples, bands, buf_row0, buf_rows,
+                             row_begin, row_end, requests, n_requests, d_status, err,
+                             static_cast<cudaStream_t>(stream));
+}
+
+hsad_status hsad_detect(const void* d_cube, int32_t elem_bytes, int64_t lines, int64_t samples,
+                        int32_t bands, const hsad_detect_request* request, hsad_pixel_error* err,
+                        void* stream) {
+    return detect_multi_impl(d_cube, elem_bytes, lines, samples, bands, 0, lines, 0, lines,
+                             request, 1, nullptr, err, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

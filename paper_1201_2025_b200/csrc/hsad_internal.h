@@ -1,0 +1,50 @@
+// Internal helpers shared by the hsad B200 translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hsad_gpu.h"
+
+namespace hsad_b200 {
+
+// Thread-local "<Name>: message" of the last failure (error.hpp:36-45 format).
+hsad_status set_error(hsad_status code, const std::string& message);
+const char* status_name(int32_t code);
+
+// Maps a CUDA runtime failure to HSAD_E_CUDA with the CUDA error text.
+hsad_status cuda_fail(cudaError_t e, const char* what);
+
+#define HSAD_CUDA_TRY(expr)                                              \
+    do {                                                                 \
+        cudaError_t e__ = (expr);                                        \
+        if (e__ != cudaSuccess) return ::hsad_b200::cuda_fail(e__, #expr); \
+    } while (0)
+
+// Reflection index, detect.cpp:71-76 (host + device).
+__host__ __device__ inline int64_t mirror_index(int64_t i, int64_t n) {
+    if (n == 1) return 0;
+    const int64_t period = 2 * (n - 1);
+    i = i < 0 ? -i : i;
+    i %= period;
+    return i < n ? i : period - i;
+}
+
+// Validation of wavelet parameters exactly as wavelet.cpp:51-56 / 122-167 raise
+// them for a pixel of `bands` samples; fills the composed target x bands
+// linear map (row-major, fp64) when `map` is non-null.
+hsad_status wavelet_plan(int32_t bands, int32_t order, int32_t target, std::vector<double>* map);
+
+hsad_status window_validate(const hsad_window& w);
+
+// Kernel-side limits.
+constexpr int kMaxDetectBands = 8;
+constexpr int kMaxBoxes = 4;
+constexpr int kMaxRequests = 4;
+constexpr int kMaxRadius = 112;  // window edge <= 225 (block of 256 columns)
+constexpr int kMaxReduceBands = 4096;
+
+}  // namespace hsad_b200

@@ -1,0 +1,283 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the pinned CPU oracle.
+
+Tolerances (BASELINE north star): DWT coefficients 1e-5 relative (we hold 1e-12),
+detector scores 1e-9 relative on the fp64 path and 1e-4 on the fp32 path, with the
+reference's rel_diff |a-b|/max(1,|a|,|b|) (proj/tests/support/testutil.hpp:34-36);
+DWEST eigen-counts and top-k anomaly sets identical. Run on a B200: pytest -m gpu.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import OracleError, max_rel_diff  # noqa: E402
+
+hs = pytest.importorskip("paper_1201_2025_b200")
+from harness.scene import CONFIGS, generate_scene  # noqa: E402
+
+DEV = "cuda:0"
+TOL64 = 1e-9
+
+
+def gpu(a):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def run(cube_np, reqs, **kw):
+    outs = hs.detect_multi(gpu(cube_np), reqs, **kw)
+    torch.cuda.synchronize()
+    return [(host(s), None if c is None else host(c)) for s, c in outs]
+
+
+def W1(n):
+    return hs.WindowConfig.single(n)
+
+
+def W2(i, o):
+    return hs.WindowConfig.dual(i, o)
+
+
+# ------------------------------------------------------------------ reduction
+@pytest.mark.parametrize("bands,order,target", [(189, 2, 4), (224, 2, 4), (64, 2, 4), (50, 3, 4),
+                                                (189, 1, 8), (16, 2, 2), (189, 2, 16), (300, 2, 4),
+                                                (224, 10, 16)])
+def test_reduce_matches_oracle(orc, bands, order, target):
+    cube = orc.port.random_cube(9, 13, bands, 1000 + bands + order)
+    want = orc.port.reduce_cube(cube, order, target)
+    for dtype in (np.float64, np.float32):
+        c = cube.astype(dtype)
+        got = host(hs.reduce_cube(gpu(c), order, target))
+        want_c = orc.port.reduce_cube(c, order, target)
+        assert max_rel_diff(got, want_c) < 1e-12
+    got32 = host(hs.reduce_cube(gpu(cube), order, target, out_dtype=torch.float32))
+    assert np.all(np.abs(got32 - want) <= 1e-6 * np.maximum(1, np.abs(want)))
+
+
+def test_reduce_constant_and_contract(orc):
+    got = host(hs.reduce_cube(gpu(np.full((3, 4, 64), 0.5)), 2, 4))
+    assert np.all(np.abs(got - 2.0) < 1e-10)
+    for order, target, name in ((2, 3, "InvalidValue"), (0, 4, "UnsupportedOrder"),
+                                (2, 512, "TargetTooLarge"), (10, 4, "TooShort")):
+        with pytest.raises(hs.HsadError) as e:
+            hs.reduce_cube(gpu(np.zeros((2, 2, 189))), order, target)
+        assert e.value.name == name
+
+
+# ------------------------------------------------------------------ reference KATs
+def _hand(center):
+    cube = np.zeros((3, 3, 2))
+    cube[0, 0] = (2, 0); cube[0, 1] = (0, 2); cube[0, 2] = (-2, 0); cube[1, 0] = (0, -2)
+    cube[1, 1] = center
+    return cube
+
+
+def test_lrx_hand_case_25():
+    m = hs.local_rx(gpu(_hand((3, 4))), W1(3), 1e-9)
+    assert abs(m.at(1, 1) - 25.0) < 25e-6 and m.algorithm == "lrx" and m.window == "3"
+
+
+def test_dwrx_hand_case_5():
+    assert abs(hs.dwrx(gpu(_hand((1, 2))), W2(1, 3), 1e-9).at(1, 1) - 5.0) < 5e-6
+
+
+def test_constant_fields_zero():
+    assert torch.all(hs.local_rx(gpu(np.full((6, 7, 3), 2.5)), W1(3)).scores == 0)
+    assert torch.all(hs.dwrx(gpu(np.full((8, 8, 3), 1.25)), W2(3, 7)).scores == 0)
+    m = hs.dwest(gpu(np.full((9, 9, 3), 0.75)), W2(3, 7))
+    assert torch.all(m.scores == 0) and torch.all(m.eigcount == 0)
+
+
+def test_pixel_equal_to_background_mean(orc):
+    cube = orc.port.random_cube(7, 7, 2, 5)
+    ring = [cube[3 + dr, 3 + dc] for dr in range(-2, 3) for dc in range(-2, 3) if (dr, dc) != (0, 0)]
+    cube[3, 3] = np.mean(ring, axis=0)
+    assert hs.local_rx(gpu(cube), W1(5)).at(3, 3) < 1e-18
+
+
+@pytest.mark.parametrize("seed", [2024, 0xACCE3])
+def test_random_cube_parity(orc, seed):
+    # test_detect.cpp:152-170 / acceptance criterion 3
+    cube = orc.port.random_cube(10, 10, 4, seed)
+    assert max_rel_diff(host(hs.local_rx(gpu(cube), W1(5), 1e-6).scores),
+                        orc.port.local_rx(cube, 5, 1e-6)) < 1e-10
+    assert max_rel_diff(host(hs.dwrx(gpu(cube), W2(3, 7), 1e-6).scores),
+                        orc.port.dwrx(cube, 3, 7, 1e-6)) < 1e-10
+    m = hs.dwest(gpu(cube), W2(3, 7))
+    s, n = orc.port.dwest(cube, 3, 7, 0.1)
+    assert max_rel_diff(host(m.scores), s) < 1e-10
+    assert np.array_equal(host(m.eigcount), n)
+
+
+def test_against_reference_naive_oracles(ref, orc):
+    cube = orc.port.random_cube(10, 10, 4, 2024)
+    assert max_rel_diff(host(hs.local_rx(gpu(cube), W1(5)).scores), ref.naive_lrx(cube, 5, 1e-6)) < 1e-10
+    assert max_rel_diff(host(hs.dwrx(gpu(cube), W2(3, 7)).scores), ref.naive_dwrx(cube, 3, 7, 1e-6)) < 1e-10
+    assert max_rel_diff(host(hs.dwest(gpu(cube), W2(3, 7)).scores), ref.naive_dwest(cube, 3, 7, 0.1)) < 1e-10
+
+
+@pytest.mark.parametrize("bands", [1, 2, 3, 4, 5, 6, 8])
+def test_band_counts(orc, bands):
+    cube = orc.port.random_cube(12, 17, bands, 300 + bands)
+    (l, _), (d, _), (e, n) = run(cube, [hs.DetectRequest("lrx", W1(5)),
+                                       hs.DetectRequest("dwrx", W2(3, 7)),
+                                       hs.DetectRequest("dwest", W2(3, 7), eigcount=True)])
+    assert max_rel_diff(l, orc.port.local_rx(cube, 5)) < TOL64
+    assert max_rel_diff(d, orc.port.dwrx(cube, 3, 7)) < TOL64
+    s, c = orc.port.dwest(cube, 3, 7)
+    assert max_rel_diff(e, s) < TOL64 and np.array_equal(n, c)
+
+
+@pytest.mark.parametrize("window,inner,outer", [(3, 1, 3), (7, 3, 9), (11, 5, 11), (15, 5, 15),
+                                                (21, 7, 21), (25, 3, 25)])
+def test_window_sizes_and_borders(orc, window, inner, outer):
+    # images smaller than the window exercise the folding reflection (detect.cpp:71-76)
+    for shape in ((23, 31), (6, 9), (40, 5)):
+        cube = orc.port.random_cube(*shape, 4, window * 7 + shape[0])
+        (l, _), (d, _) = run(cube, [hs.DetectRequest("lrx", W1(window)),
+                                    hs.DetectRequest("dwrx", W2(inner, outer))])
+        assert max_rel_diff(l, orc.port.local_rx(cube, window)) < TOL64
+        assert max_rel_diff(d, orc.port.dwrx(cube, inner, outer)) < TOL64
+        if inner > 1:
+            (e, n), = run(cube, [hs.DetectRequest("dwest", W2(inner, outer), eigcount=True)])
+            s, c = orc.port.dwest(cube, inner, outer)
+            assert max_rel_diff(e, s) < TOL64 and np.array_equal(n, c)
+
+
+def test_lrx_guard_extension(orc):
+    cube = orc.port.random_cube(20, 21, 4, 9)
+    (g, _), = run(cube, [hs.DetectRequest("lrx", W1(9), guard=3)])
+    assert max_rel_diff(g, orc.port.local_rx(cube, 9, 1e-6, guard=3)) < TOL64
+
+
+def test_properties(orc):
+    cube = orc.port.random_cube(8, 8, 3, 31)
+    sh = cube + np.array([5.0, -2.0, 11.0])
+    for f in (lambda c: hs.local_rx(c, W1(5)), lambda c: hs.dwrx(c, W2(3, 7)),
+              lambda c: hs.dwest(c, W2(3, 7))):
+        a, b = host(f(gpu(cube)).scores), host(f(gpu(sh)).scores)
+        assert max_rel_diff(a, b) < 1e-8 and np.all(np.isfinite(a)) and np.all(a >= 0)
+    c4 = orc.port.random_cube(8, 8, 4, 41)
+    B = np.array([[2, .5, 0, .1], [0, 1.5, .3, 0], [.2, 0, 1, .4], [0, .1, 0, .8]])
+    assert max_rel_diff(host(hs.local_rx(gpu(c4), W1(5), 0.0).scores),
+                        host(hs.local_rx(gpu(c4 @ B.T), W1(5), 0.0).scores)) < 1e-6
+
+
+def test_chi_square_global_rx():
+    # acceptance criterion 4: global RX (window 101, ridge 0) on iid Gaussian, mean ~ L
+    g = torch.Generator().manual_seed(0xACCE4)
+    cube = 0.5 + 0.1 * torch.randn((101, 101, 8), generator=g, dtype=torch.float64)
+    m = hs.local_rx(cube.to(DEV), W1(101), 0.0)
+    assert abs(float(m.scores.mean()) - 8.0) / 8.0 < 0.05
+
+
+def test_dispatch_and_errors(orc):
+    cube = gpu(orc.port.random_cube(8, 8, 3, 61))
+    assert hs.detect(cube, "lrx", W1(5)).algorithm == "lrx"
+    for algo, w in (("dwest", W1(15)), ("lrx", W2(3, 7)), ("dwrx", W1(5))):
+        with pytest.raises(hs.HsadError) as e:
+            hs.detect(cube, algo, w)
+        assert e.value.name == "ConfigMismatch"
+    with pytest.raises(hs.HsadError) as e:
+        hs.dwest(cube, W2(1, 5))
+    assert e.value.name == "TooFewSamples" and "at pixel (0, 0)" in str(e.value)
+
+
+def test_singular_pixel_error_matches_oracle(orc):
+    cube = np.zeros((5, 5, 2)); cube[2, 2] = (1.0, 1.0)
+    with pytest.raises(OracleError) as want:
+        orc.port.local_rx(cube, 3, 1e-6)
+    with pytest.raises(hs.HsadError) as got:
+        hs.local_rx(gpu(cube), W1(3), 1e-6)
+    assert got.value.name == want.value.name == "SingularAfterRidge"
+    assert (got.value.row, got.value.col) == (want.value.row, want.value.col)
+    assert str(got.value) == str(want.value)
+
+
+# ------------------------------------------------------------------ BASELINE configs
+def _pipeline_check(orc, name, reqs_spec, order=2, rows=None):
+    cfg = CONFIGS[name]
+    cube, truth = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"],
+                                 cfg["rate"], device=DEV)
+    red = hs.reduce_cube(cube, order, 4)
+    cube_h = host(cube)
+    red_o = orc.port.reduce_cube(cube_h, order, 4, workers=8)
+    assert max_rel_diff(host(red), red_o) < 1e-12
+    reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in reqs_spec]
+    outs = hs.detect_multi(red, reqs)
+    torch.cuda.synchronize()
+    k = int(truth.sum())
+    for (a, w, kw), (s, c) in zip(reqs_spec, outs):
+        s = host(s)
+        if a == "lrx":
+            want = orc.port.local_rx(red_o, w.single_size, 1e-6, guard=kw.get("guard", 1), workers=8)
+        elif a == "dwrx":
+            want = orc.port.dwrx(red_o, w.inner_size, w.outer_size, 1e-6, workers=8)
+        else:
+            want, wc = orc.port.dwest(red_o, w.inner_size, w.outer_size, 0.1, workers=8)
+            assert np.array_equal(host(c), wc), f"{name} {a} eigen-counts"
+        assert max_rel_diff(s, want) < TOL64, f"{name} {a}"
+        top_g = set(np.argsort(-s.ravel(), kind="stable")[:k].tolist())
+        top_o = set(np.argsort(-want.ravel(), kind="stable")[:k].tolist())
+        assert top_g == top_o, f"{name} {a} top-{k}"
+
+
+def test_config_c1(orc):
+    _pipeline_check(orc, "C1", [("lrx", W1(9), {"guard": 3}), ("lrx", W1(9), {})])
+
+
+def test_config_c2(orc):
+    _pipeline_check(orc, "C2", [("dwrx", W2(5, 11), {}), ("dwest", W2(5, 11), {})])
+
+
+def test_config_c4(orc):
+    _pipeline_check(orc, "C4", [("lrx", W1(11), {}), ("dwrx", W2(5, 11), {}),
+                                ("dwest", W2(5, 11), {})])
+
+
+# ------------------------------------------------------------------ sharding / e2e
+def test_strip_split_bit_identical(orc):
+    cube = gpu(orc.port.random_cube(200, 150, 4, 77))
+    reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwrx", W2(5, 11)),
+            hs.DetectRequest("dwest", W2(5, 11), eigcount=True)]
+    whole = hs.detect_multi(cube, reqs)
+    q = hs.row_quantum(200, 150)
+    for g in (2, 4, 8):
+        per = -(-200 // (g * q)) * q
+        for r0 in range(0, 200, per):
+            r1 = min(200, r0 + per)
+            b0, nb = hs.strip_rows(200, r0, r1, reqs)
+            part = hs.detect_multi(cube[b0:b0 + nb], reqs, lines=200, buf_row0=b0,
+                                   row_begin=r0, row_end=r1)
+            for (ws, wc), (ps, pc) in zip(whole, part):
+                assert torch.equal(ws[r0:r1], ps)
+                if wc is not None:
+                    assert torch.equal(wc[r0:r1], pc)
+
+
+def test_pipeline_host_equals_device_path(orc):
+    cfg = CONFIGS["C2"]
+    cube, _ = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], cfg["rate"])
+    h = cube.contiguous().pin_memory()
+    reqs = [hs.DetectRequest("dwrx", W2(5, 11)), hs.DetectRequest("dwest", W2(5, 11), eigcount=True),
+            hs.DetectRequest("lrx", W1(11), score_dtype=torch.float32)]
+    outs = [(torch.empty((100, 100), dtype=r.score_dtype).pin_memory(),
+             torch.empty((100, 100), dtype=torch.int8) if r.eigcount else None) for r in reqs]
+    hs.pipeline_host(h, 2, 4, reqs, outs)
+    dev = hs.detect_multi(hs.reduce_cube(cube.to(DEV), 2, 4), reqs)
+    for (a, ac), (b, bc) in zip(outs, dev):
+        assert torch.equal(a, b.cpu())
+        if ac is not None:
+            assert torch.equal(ac, bc.cpu())
+    # fp32 path: within 1e-4 of the fp64 oracle
+    red_o = orc.port.reduce_cube(host(cube), 2, 4)
+    assert max_rel_diff(outs[2][0].numpy().astype(np.float64), orc.port.local_rx(red_o, 11)) < 1e-4
+
+
+def test_cpu_tensor_rejected():
+    with pytest.raises(TypeError):
+        hs.reduce_cube(torch.zeros((2, 2, 8)), 2, 4)
