@@ -126,12 +126,23 @@ __device__ __forceinline__ int tri(int i, int j) {  // packed upper index, i <= 
     return L + i * L - i * (i - 1) / 2 + (j - i);
 }
 
+// fp64 reciprocal: MUFU seed + two Newton steps (~1 ulp; the IEEE divide is a
+// 20-instruction subroutine and nothing here needs correct rounding).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
 // mean and covariance (divisor N) from box sums: C = S2/N - mu mu^T
 // (== stats.cpp:13-29 in exact arithmetic on the shifted values)
 template <int L>
 __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n, double (&mu)[L],
                                          double (&c)[L][L]) {
-    const double inv = 1.0 / n;
+    const double inv = fast_rcp(n);
 #pragma unroll
     for (int i = 0; i < L; ++i) mu[i] = s[i] * inv;
 #pragma unroll
@@ -147,14 +158,16 @@ __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n
 // regularized_inverse + quadratic form (stats.cpp:31-62, detect.cpp:179-180):
 // delta = ridge tr(C)/L, Cholesky of C + delta I, score = |L^-1 d|^2.
 // Singular rule on the pivots D_j = L_jj^2 (stats.cpp:45-48): a non-positive
-// pivot, or min D <= 1e-14 max D. Returns 0 or an error code.
+// pivot, or min D <= 1e-14 max D. Only 1/L_jj is ever needed, so each column
+// costs one fp64 rsqrt (MUFU seed + Newton) instead of an IEEE sqrt + divide.
+// Returns 0 or an error code.
 template <int L>
 __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L], double ridge,
                                          double& score, double& delta) {
     double tr = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i) tr += a[i][i];
-    delta = ridge * tr / static_cast<double>(L);
+    delta = (L & (L - 1)) == 0 ? ridge * tr * (1.0 / L) : ridge * tr / static_cast<double>(L);
 #pragma unroll
     for (int i = 0; i < L; ++i) a[i][i] += delta;
     double dmax = 0.0, dmin = DBL_MAX;
@@ -168,9 +181,7 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
         ok = ok && (p > 0.0);
         dmax = fmax(dmax, fabs(p));
         dmin = fmin(dmin, p);
-        const double ljj = sqrt(fmax(p, 0.0));
-        const double rinv = 1.0 / ljj;
-        a[j][j] = ljj;
+        const double rinv = rsqrt(fmax(p, DBL_MIN));
 #pragma unroll
         for (int i = j + 1; i < L; ++i) {
             double v = a[i][j];
@@ -192,72 +203,139 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
     return 0;
 }
 
-// symmetric_eigen (stats.cpp:64-89): cyclic Jacobi with tan-half-angle updates
-// to full fp64 accuracy; descending order (stable), eigenvector sign so that its
-// first largest-|.| component is positive.
+// One Jacobi rotation zeroing a[p][q]; tan-half-angle form (Rutishauser).
+template <int L, typename T>
+__device__ __forceinline__ void rotate(T (&a)[L][L], T (&v)[L][L], int p, int q, T t) {
+    const T apq = a[p][q];
+    const T c = rsqrt(T(1) + t * t);
+    const T s = t * c;
+    a[p][p] -= t * apq;
+    a[q][q] += t * apq;
+    a[p][q] = T(0);
+    a[q][p] = T(0);
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        if (k == p || k == q) continue;
+        const T akp = a[k][p], akq = a[k][q];
+        const T nkp = c * akp - s * akq;
+        const T nkq = s * akp + c * akq;
+        a[k][p] = nkp;
+        a[p][k] = nkp;
+        a[k][q] = nkq;
+        a[q][k] = nkq;
+    }
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        const T vkp = v[k][p], vkq = v[k][q];
+        v[k][p] = c * vkp - s * vkq;
+        v[k][q] = s * vkp + c * vkq;
+    }
+}
+
+// tan of the Jacobi angle for the pair (p, q): t = sgn(th)/(|th| + sqrt(th^2 + 1)),
+// th = (a_qq - a_pp) / (2 a_pq); for |a_pq| << |a_qq - a_pp| the series
+// t = x (1 - x^2), x = a_pq / (a_qq - a_pp), is exact to fp64 when |x| < 1e-4.
+__device__ __forceinline__ float jacobi_t(float app, float aqq, float apq) {
+    const float th = 0.5f * (aqq - app) / apq;
+    const float t = 1.0f / (fabsf(th) + sqrtf(fmaf(th, th, 1.0f)));
+    return th < 0.0f ? -t : t;
+}
+__device__ __forceinline__ double jacobi_t(double app, double aqq, double apq) {
+    const double h = aqq - app;
+    if (fabs(apq) < 1e-4 * fabs(h)) {
+        const double x = apq * fast_rcp(h);
+        return x * fma(-x, x, 1.0);
+    }
+    const double th = 0.5 * h * fast_rcp(apq);
+    const double r = fma(th, th, 1.0);
+    const double t = fast_rcp(fabs(th) + r * rsqrt(r));
+    return th < 0.0 ? -t : t;
+}
+
+// symmetric_eigen (stats.cpp:64-89) for the small DWEST matrix.
+//   1. cyclic Jacobi in fp32 on the max-normalised matrix (4 sweeps): the cheap
+//      part of the work, MUFU rcp/rsqrt;
+//   2. fp64 modified Gram-Schmidt of those vectors -> exactly orthonormal Q,
+//      B = Q^T A Q in fp64 (off-diagonal ~1e-7 |A|);
+//   3. two fp64 Jacobi sweeps on B (quadratic convergence: 1e-7 -> 1e-14 -> 1e-28),
+//      accumulated into Q.
+// Then descending order (stable on ties) and the sign rule: the first
+// largest-|.| component of each eigenvector is made positive.
 template <int L>
-__device__ __forceinline__ void jacobi_eigen(double (&a)[L][L], double (&v)[L][L], double (&w)[L]) {
+__device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)[L][L], double (&w)[L]) {
+    double amax = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
-        for (int j = 0; j < L; ++j) v[i][j] = i == j ? 1.0 : 0.0;
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        double off = 0.0;
+        for (int j = 0; j < L; ++j) amax = fmax(amax, fabs(A[i][j]));
+    const double scale = amax > 0.0 ? fast_rcp(amax) : 1.0;
+    float a32[L][L], v32[L][L];
 #pragma unroll
-        for (int p = 0; p < L; ++p)
+    for (int i = 0; i < L; ++i)
 #pragma unroll
-            for (int q = p + 1; q < L; ++q) off += fabs(a[p][q]);
-        if (off == 0.0) break;
+        for (int j = 0; j < L; ++j) {
+            a32[i][j] = static_cast<float>(A[i][j] * scale);
+            v32[i][j] = i == j ? 1.0f : 0.0f;
+        }
+#pragma unroll 1
+    for (int sweep = 0; sweep < 4; ++sweep) {
 #pragma unroll
         for (int p = 0; p < L - 1; ++p)
 #pragma unroll
-            for (int q = p + 1; q < L; ++q) {
-                const double apq = a[p][q];
-                const double g = 100.0 * fabs(apq);
-                if (sweep > 3 && fabs(a[p][p]) + g == fabs(a[p][p]) &&
-                    fabs(a[q][q]) + g == fabs(a[q][q])) {
-                    a[p][q] = 0.0;
-                    a[q][p] = 0.0;
-                } else if (apq != 0.0) {
-                    const double h = a[q][q] - a[p][p];
-                    double t;
-                    if (fabs(h) + g == fabs(h)) {
-                        t = apq / h;
-                    } else {
-                        const double theta = 0.5 * h / apq;
-                        t = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
-                        if (theta < 0.0) t = -t;
-                    }
-                    const double c = 1.0 / sqrt(1.0 + t * t);
-                    const double s = t * c;
-                    const double tau = s / (1.0 + c);
-                    a[p][p] -= t * apq;
-                    a[q][q] += t * apq;
-                    a[p][q] = 0.0;
-                    a[q][p] = 0.0;
+            for (int q = p + 1; q < L; ++q)
+                if (a32[p][q] != 0.0f) rotate<L, float>(a32, v32, p, q, jacobi_t(a32[p][p], a32[q][q], a32[p][q]));
+    }
+    // modified Gram-Schmidt in fp64
 #pragma unroll
-                    for (int k = 0; k < L; ++k) {
-                        if (k == p || k == q) continue;
-                        const double akp = a[k][p], akq = a[k][q];
-                        const double nkp = akp - s * (akq + tau * akp);
-                        const double nkq = akq + s * (akp - tau * akq);
-                        a[k][p] = nkp;
-                        a[p][k] = nkp;
-                        a[k][q] = nkq;
-                        a[q][k] = nkq;
-                    }
+    for (int j = 0; j < L; ++j) {
 #pragma unroll
-                    for (int k = 0; k < L; ++k) {
-                        const double vkp = v[k][p], vkq = v[k][q];
-                        v[k][p] = vkp - s * (vkq + tau * vkp);
-                        v[k][q] = vkq + s * (vkp - tau * vkq);
-                    }
-                }
-            }
+        for (int k = 0; k < L; ++k) V[k][j] = static_cast<double>(v32[k][j]);
+#pragma unroll
+        for (int i = 0; i < j; ++i) {
+            double dot = 0.0;
+#pragma unroll
+            for (int k = 0; k < L; ++k) dot = fma(V[k][i], V[k][j], dot);
+#pragma unroll
+            for (int k = 0; k < L; ++k) V[k][j] = fma(-dot, V[k][i], V[k][j]);
+        }
+        double nrm = 0.0;
+#pragma unroll
+        for (int k = 0; k < L; ++k) nrm = fma(V[k][j], V[k][j], nrm);
+        const double r = rsqrt(nrm);
+#pragma unroll
+        for (int k = 0; k < L; ++k) V[k][j] *= r;
+    }
+    // B = V^T A V
+    double AV[L][L], B[L][L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < L; ++k) acc = fma(A[i][k], V[k][j], acc);
+            AV[i][j] = acc;
+        }
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < L; ++k) acc = fma(V[k][i], AV[k][j], acc);
+            B[i][j] = acc;
+            B[j][i] = acc;
+        }
+#pragma unroll 1
+    for (int sweep = 0; sweep < 2; ++sweep) {
+#pragma unroll
+        for (int p = 0; p < L - 1; ++p)
+#pragma unroll
+            for (int q = p + 1; q < L; ++q)
+                if (B[p][q] != 0.0) rotate<L, double>(B, V, p, q, jacobi_t(B[p][p], B[q][q], B[p][q]));
     }
 #pragma unroll
-    for (int i = 0; i < L; ++i) w[i] = a[i][i];
-    // stable descending bubble sort of (w, columns of v)
+    for (int i = 0; i < L; ++i) w[i] = B[i][i];
 #pragma unroll
     for (int pass = 0; pass < L - 1; ++pass)
 #pragma unroll
@@ -268,9 +346,9 @@ __device__ __forceinline__ void jacobi_eigen(double (&a)[L][L], double (&v)[L][L
                 w[i + 1] = tw;
 #pragma unroll
                 for (int k = 0; k < L; ++k) {
-                    const double tv = v[k][i];
-                    v[k][i] = v[k][i + 1];
-                    v[k][i + 1] = tv;
+                    const double tv = V[k][i];
+                    V[k][i] = V[k][i + 1];
+                    V[k][i + 1] = tv;
                 }
             }
         }
@@ -279,15 +357,15 @@ __device__ __forceinline__ void jacobi_eigen(double (&a)[L][L], double (&v)[L][L
         double best = -1.0, val = 0.0;
 #pragma unroll
         for (int k = 0; k < L; ++k) {
-            const double av = fabs(v[k][i]);
+            const double av = fabs(V[k][i]);
             if (av > best) {
                 best = av;
-                val = v[k][i];
+                val = V[k][i];
             }
         }
         if (val < 0.0) {
 #pragma unroll
-            for (int k = 0; k < L; ++k) v[k][i] = -v[k][i];
+            for (int k = 0; k < L; ++k) V[k][i] = -V[k][i];
         }
     }
 }
@@ -378,7 +456,11 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
         shifted(r, yc);
 
         for (int q = 0; q < P.nreq; ++q) {
-            const ReqDev& R = P.req[q];
+            // static indices only: a dynamic P.req[q] spills the param array to the stack
+            ReqDev R = P.req[0];
+#pragma unroll
+            for (int qq = 1; qq < kMaxRequests; ++qq)
+                if (q == qq) R = P.req[qq];
             if (R.algo == HSAD_LRX) {
                 // detect.cpp:168-188: background = box - centre (or - guard box)
                 double bg[NC];
@@ -469,7 +551,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
                     for (int i = 0; i < L; ++i)
 #pragma unroll
                         for (int j = 0; j < L; ++j) cd[i][j] = c_in[i][j] - c_out[i][j];
-                    jacobi_eigen<L>(cd, vec, w);
+                    dwest_eigen<L>(cd, vec, w);
                     double score = 0.0;
                     int count = 0;
                     const double lmax = w[0];

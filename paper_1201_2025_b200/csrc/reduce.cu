@@ -92,6 +92,129 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-staged variant (the default path). A persistent CTA of 8 warps streams
+// contiguous tiles of P pixels (P*L*elem bytes, one TMA bulk copy each) through
+// a 3-stage shared-memory ring guarded by mbarriers, so ~2 tiles (>100 KB) per SM
+// are always in flight regardless of register pressure. Warps consume a stage
+// exactly like the lane-split kernel, reading the spectra from shared memory
+// (lane l reads band l + 32 s: consecutive words, conflict-free for any L).
+constexpr int kStages = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <typename Tin, int TARGET, int BPL>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    reduce_bulk_kernel(const Tin* __restrict__ cube, int64_t npix, int bands, int tile_px,
+                       const double* __restrict__ wmap, void* __restrict__ out, int out_bytes) {
+    constexpr int G = 32 / TARGET;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+    Tin* stage0 = reinterpret_cast<Tin*>(smem_raw + 128);
+    const int64_t stage_elems = static_cast<int64_t>(tile_px) * bands;
+    const uint32_t tile_bytes = static_cast<uint32_t>(stage_elems * sizeof(Tin));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    double w[BPL][TARGET];
+#pragma unroll
+    for (int s = 0; s < BPL; ++s) {
+        const int b = lane + 32 * s;
+#pragma unroll
+        for (int k = 0; k < TARGET; ++k) w[s][k] = b < bands ? wmap[k * bands + b] : 0.0;
+    }
+
+    const int64_t full_tiles = npix / tile_px;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            const int64_t t = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
+            if (t < full_tiles) {
+                mbar_expect_tx(&bars[s], tile_bytes);
+                bulk_g2s(stage0 + s * stage_elems, cube + t * stage_elems, tile_bytes, &bars[s]);
+            }
+        }
+    }
+    const int groups = tile_px / G;
+    int64_t k = 0;
+    for (int64_t t = blockIdx.x; t < full_tiles; t += gridDim.x, ++k) {
+        const int s = static_cast<int>(k % kStages);
+        mbar_wait(&bars[s], static_cast<uint32_t>((k / kStages) & 1));
+        const Tin* tile = stage0 + s * stage_elems;
+        for (int gi = warp; gi < groups; gi += kWarps) {
+            double v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                const Tin* px = tile + static_cast<int64_t>(gi * G + j) * bands;
+                double x[BPL];
+#pragma unroll
+                for (int s2 = 0; s2 < BPL; ++s2) {
+                    const int b = lane + 32 * s2;
+                    x[s2] = b < bands ? static_cast<double>(px[b]) : 0.0;
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < BPL; ++s2)
+#pragma unroll
+                    for (int kk = 0; kk < TARGET; ++kk)
+                        v[j * TARGET + kk] = fma(w[s2][kk], x[s2], v[j * TARGET + kk]);
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const bool upper = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < o; ++i) {
+                    const double send = upper ? v[i] : v[i + o];
+                    const double keep = upper ? v[i + o] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            const int64_t oidx = (t * tile_px + gi * G) * TARGET + lane;
+            if (out_bytes == 8) static_cast<double*>(out)[oidx] = v[0];
+            else static_cast<float*>(out)[oidx] = static_cast<float>(v[0]);
+        }
+        __syncthreads();  // every warp is done with stage s
+        if (threadIdx.x == 0) {
+            const int64_t tn = t + static_cast<int64_t>(kStages) * gridDim.x;
+            if (tn < full_tiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bars[s], tile_bytes);
+                bulk_g2s(stage0 + s * stage_elems, cube + tn * stage_elems, tile_bytes, &bars[s]);
+            }
+        }
+    }
+}
+
 // Fallback for targets > 8 or very long spectra: one thread per output value.
 template <typename Tin>
 __global__ void reduce_generic_kernel(const Tin* __restrict__ cube, int64_t npix, int bands,
@@ -120,25 +243,64 @@ int grid_for(int64_t work_items, int per_block) {
     return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
+int device_sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Pixels per bulk tile: a multiple of 32 (so every warp group is full and the
+// tile start stays 16-byte aligned for any band count) with <= 64 KB per stage.
+int bulk_tile_px(int bands, int elem) {
+    int px = 64;
+    while (px > 32 && static_cast<int64_t>(px) * bands * elem > 64 * 1024) px /= 2;
+    if (static_cast<int64_t>(px) * bands * elem > 64 * 1024) return 0;
+    return px;
+}
+
+template <typename Tin, int TARGET, int B>
+cudaError_t launch_tb(const Tin* cube, int64_t npix, int bands, const double* wmap, void* out,
+                      int out_bytes, cudaStream_t s) {
+    constexpr int G = 32 / TARGET;
+    const int tile = bulk_tile_px(bands, sizeof(Tin));
+    int64_t done = 0;
+    if (tile > 0 && npix >= tile) {
+        const int64_t tiles = npix / tile;
+        const size_t smem = 128 + static_cast<size_t>(kStages) * tile * bands * sizeof(Tin);
+        auto k = reduce_bulk_kernel<Tin, TARGET, B>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const int64_t sms = device_sm_count();
+        const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+        k<<<grid, kWarps * 32, smem, s>>>(cube, npix, bands, tile, wmap, out, out_bytes);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        done = tiles * tile;
+    }
+    if (done < npix) {  // tail (and tiny cubes): direct lane-split loads
+        const int64_t rest = npix - done;
+        const int grid = grid_for((rest + G - 1) / G, kWarps);
+        reduce_lanesplit_kernel<Tin, TARGET, B><<<grid, kWarps * 32, 0, s>>>(
+            cube + done * bands, rest, bands, wmap,
+            static_cast<char*>(out) + done * TARGET * out_bytes, out_bytes);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
+}
+
 template <typename Tin, int TARGET>
 cudaError_t launch_target(const Tin* cube, int64_t npix, int bands, const double* wmap, void* out,
                           int out_bytes, cudaStream_t s) {
-    constexpr int G = 32 / TARGET;
-    const int64_t groups = (npix + G - 1) / G;
-    const int grid = grid_for(groups, kWarps);
     const int bpl = (bands + 31) / 32;
-#define HSAD_RL(B)                                                                            \
-    reduce_lanesplit_kernel<Tin, TARGET, B><<<grid, kWarps * 32, 0, s>>>(cube, npix, bands, wmap, \
-                                                                         out, out_bytes)
-    if (bpl <= 1) HSAD_RL(1);
-    else if (bpl <= 2) HSAD_RL(2);
-    else if (bpl <= 4) HSAD_RL(4);
-    else if (bpl <= 6) HSAD_RL(6);
-    else if (bpl <= 7) HSAD_RL(7);
-    else if (bpl <= 8) HSAD_RL(8);
-    else return cudaErrorInvalidValue;
-#undef HSAD_RL
-    return cudaGetLastError();
+    if (bpl <= 1) return launch_tb<Tin, TARGET, 1>(cube, npix, bands, wmap, out, out_bytes, s);
+    if (bpl <= 2) return launch_tb<Tin, TARGET, 2>(cube, npix, bands, wmap, out, out_bytes, s);
+    if (bpl <= 4) return launch_tb<Tin, TARGET, 4>(cube, npix, bands, wmap, out, out_bytes, s);
+    if (bpl <= 6) return launch_tb<Tin, TARGET, 6>(cube, npix, bands, wmap, out, out_bytes, s);
+    if (bpl <= 7) return launch_tb<Tin, TARGET, 7>(cube, npix, bands, wmap, out, out_bytes, s);
+    if (bpl <= 8) return launch_tb<Tin, TARGET, 8>(cube, npix, bands, wmap, out, out_bytes, s);
+    return cudaErrorInvalidValue;
 }
 
 template <typename Tin>
