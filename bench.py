@@ -1,0 +1,380 @@
+"""Benchmark: Mpixel/s for DWT + LRX/DWRX/DWEST scoring (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
+
+Workload (default C5, BASELINE.json configs[4]: the largest single-GPU config and the
+one the 1/2/4/8-GPU scaling and HBM roofline are quoted on): a 4096 x 4096 x 224 fp32
+BIP cube from the BASELINE generator (harness/scene.py, seeded, synthetic stand-in for
+AVIRIS), db4 DWT to 4 approximation bands, then Local RX (11x11), DWRX (5/11) and
+DWEST (5/11, + int8 eigen-count) — the fp64 path (all arithmetic fp64, fp64 score maps).
+
+One step = one pass of that hot path over the cube:
+  value : cube already resident in HBM; CUDA events around K steps of
+          hsad_reduce + hsad_detect_multi (C-ABI) on the launching stream,
+          barrier + synchronize on both sides, max over ranks;
+  e2e   : hsad_pipeline_host (C-ABI) from pinned HOST memory: H2D of the cube,
+          reduce, detectors, D2H of every map, timed per step.
+Multi-GPU (torchrun): row strips aligned to hsad_row_quantum, each rank holds its
+strip + mirror halo (generated from the same seeded row chunks = the host copy),
+computes it, and the fp64 maps are gathered to rank 0 with NCCL (dist.gather)
+inside the timed region. scaling = "strong" (the 4096^2 image is fixed).
+
+--impl reference times the CPU restatement of the reference (oracle/, the
+reference itself needs Eigen3, absent here) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+WINDOWS = {"lrx": 11, "inner": 5, "outer": 11}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        d = json.loads(PEAKS.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def requests(hs, score_dtype=torch.float64):
+    W1, W2 = hs.WindowConfig.single, hs.WindowConfig.dual
+    return [hs.DetectRequest("lrx", W1(WINDOWS["lrx"]), score_dtype=score_dtype),
+            hs.DetectRequest("dwrx", W2(WINDOWS["inner"], WINDOWS["outer"]), score_dtype=score_dtype),
+            hs.DetectRequest("dwest", W2(WINDOWS["inner"], WINDOWS["outer"]), eigcount=True,
+                             score_dtype=score_dtype)]
+
+
+def bytes_per_pixel(bands: int) -> int:
+    # algorithmic: read the fp32 spectrum once, write three fp64 maps + int8 eigen-count
+    return 4 * bands + 3 * 8 + 1
+
+
+def cpu_baseline(cube_rows_np: np.ndarray, lines: int, rows_total: int, budget_s: float):
+    """Oracle port (the CPU restatement of proj/core/src/{wavelet,detect,stats}.cpp)
+    on a bounded row sample of the same cube, all host threads."""
+    import oracle
+    cores = os.cpu_count() or 1
+    L = cube_rows_np.shape[0]
+    # the sample: rows [0, n) of the workload, DWT of the rows the windows need
+    def run(n):
+        t0 = time.perf_counter()
+        need = min(L, n + WINDOWS["outer"])
+        red = oracle.port.reduce_cube(cube_rows_np[:need], 2, 4, workers=cores)
+        oracle.port.local_rx(red, WINDOWS["lrx"], 1e-6, workers=cores, rows=(0, n))
+        oracle.port.dwrx(red, WINDOWS["inner"], WINDOWS["outer"], 1e-6, workers=cores, rows=(0, n))
+        oracle.port.dwest(red, WINDOWS["inner"], WINDOWS["outer"], 0.1, workers=cores, rows=(0, n))
+        return time.perf_counter() - t0
+    n = 8
+    dt = run(n)
+    n = int(max(8, min(L - WINDOWS["outer"], n * budget_s / max(dt, 1e-3))))
+    dt = run(n)
+    px = n * cube_rows_np.shape[1]
+    return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "port",
+            "sample": f"rows 0..{n} of the workload ({px} px; DWT on {min(L, n + WINDOWS['outer'])} rows "
+                      f"+ LRX/DWRX/DWEST), {dt:.1f} s, oracle/hsad_oracle.cpp with {cores} threads"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU restatement of the reference path on the host cores."""
+    if rank != 0:
+        return
+    from harness.scene import generate_rows
+    sample_rows = 48
+    cube = generate_rows(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], 0,
+                         sample_rows + WINDOWS["outer"], cfg["rate"], device="cpu").numpy()
+    import oracle
+    cores = os.cpu_count() or 1
+    n = sample_rows
+
+    def step():
+        red = oracle.port.reduce_cube(cube, 2, 4, workers=cores)
+        oracle.port.local_rx(red, WINDOWS["lrx"], 1e-6, workers=cores, rows=(0, n))
+        oracle.port.dwrx(red, WINDOWS["inner"], WINDOWS["outer"], 1e-6, workers=cores, rows=(0, n))
+        oracle.port.dwest(red, WINDOWS["inner"], WINDOWS["outer"], 0.1, workers=cores, rows=(0, n))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    px = n * cfg["samples"]
+    v = px / dt / 1e6
+    line = {
+        "impl": "reference", "metric": "Mpixels/sec for DWT+LRX/DWRX/DWEST scoring",
+        "value": v, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, cfg),
+        "cpu_baseline": {"value": v, "unit": "Mpixel/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} rows x {cfg['samples']} cols per step (DWT + 3 detectors) of the "
+                                   "workload; CPU restatement (the reference needs Eigen3, absent)"},
+        "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, cfg):
+    return {"workload": f"{args.config}: {cfg['lines']}x{cfg['samples']}x{cfg['bands']} fp32 BIP, "
+                        f"db4 DWT->4 bands + LRX {WINDOWS['lrx']} + DWRX/DWEST "
+                        f"{WINDOWS['inner']}/{WINDOWS['outer']} (+eigen-count), fp64 maps",
+            "lines": cfg["lines"], "samples": cfg["samples"], "bands": cfg["bands"],
+            "seed": cfg["seed"], "anomaly_rate": cfg["rate"],
+            "l2": "inputs larger than L2 (15 GB cube vs 126 MB L2)" if args.config == "C5"
+                  else "see note: L2 flushed between steps"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from harness.scene import CONFIGS
+    cfg = CONFIGS[args.config]
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    run_b200(args, cfg, rank, world, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_b200(args, cfg, rank, world, local, dist):
+    import paper_1201_2025_b200 as hs
+    from harness.scene import generate_rows
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    lines, samples, bands = cfg["lines"], cfg["samples"], cfg["bands"]
+    reqs = requests(hs)
+
+    # ---- row strip of this rank (aligned to the detector row quantum) + halo
+    q = hs.row_quantum(lines, samples)
+    per = -(-lines // (world * q)) * q
+    r0, r1 = min(lines, rank * per), min(lines, (rank + 1) * per)
+    b0, nb = hs.strip_rows(lines, r0, r1, reqs)
+    cube = generate_rows(lines, samples, bands, cfg["seed"], b0, b0 + nb, cfg["rate"], device=dev)
+    red = torch.empty((nb, samples, 4), dtype=torch.float64, device=dev)
+    outs = [(torch.empty((r1 - r0, samples), dtype=torch.float64, device=dev),
+             torch.empty((r1 - r0, samples), dtype=torch.int8, device=dev) if r.eigcount else None)
+            for r in reqs]
+    status = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    gathered = None
+    if world > 1 and rank == 0:
+        gathered = [[torch.empty((per, samples), dtype=torch.float64, device=dev) for _ in range(world)]
+                    for _ in reqs]
+    send_bufs = [torch.zeros((per, samples), dtype=torch.float64, device=dev) for _ in reqs]
+
+    lib = hs._abi.lib()
+    import ctypes as C
+    stream = torch.cuda.current_stream(dev)
+    creqs = (hs._abi.Request * len(reqs))(*[
+        hs.hsad._make_request(r, sc, cnt) for r, (sc, cnt) in zip(reqs, outs)])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    kern_ms = {"reduce": [], "detect": []}
+
+    def step(record=False):
+        st = lib.hsad_reduce(cube.data_ptr(), 4, nb, samples, bands, 2, 4, red.data_ptr(), 8,
+                             stream.cuda_stream)
+        assert st == 0, lib.hsad_last_error_message()
+        if record:
+            ev[1].record(stream)
+        st = lib.hsad_detect_multi(red.data_ptr(), 8, lines, samples, 4, b0, nb, r0, r1, creqs,
+                                   len(reqs), status.data_ptr(), None, stream.cuda_stream)
+        assert st == 0, lib.hsad_last_error_message()
+        if record:
+            ev[2].record(stream)
+        if world > 1:
+            for i, (sc, _) in enumerate(outs):
+                send_bufs[i][: r1 - r0].copy_(sc)
+                dist.gather(send_bufs[i], gathered[i] if rank == 0 else None, dst=0)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # per-kernel durations (events on the launching stream), outside the headline timing
+    for _ in range(3):
+        ev[0].record(stream)
+        step(record=True)
+        ev[2].synchronize()
+        kern_ms["reduce"].append(ev[0].elapsed_time(ev[1]))
+        kern_ms["detect"].append(ev[1].elapsed_time(ev[2]))
+
+    clocks = Clocks(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(args.steps):
+        step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    bad = int(status.item())
+    assert bad == -1, f"per-pixel failure recorded: {bad}"
+
+    # ---- end to end through the C-ABI from pinned host buffers (rank 0 strip only at N>1)
+    e2e = None
+    host_cube = None
+    if rank == 0 or world == 1:
+        host_cube = torch.empty((nb, samples, bands), dtype=torch.float32, pin_memory=True)
+        host_cube.copy_(cube)
+        host_out = [(torch.empty((nb, samples), dtype=torch.float64, pin_memory=True),
+                     torch.empty((nb, samples), dtype=torch.int8, pin_memory=True) if r.eigcount
+                     else None) for r in reqs]
+        hs.pipeline_host(host_cube, 2, 4, reqs, host_out)  # warm (allocates the device cache)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            hs.pipeline_host(host_cube, 2, 4, reqs, host_out)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        h2d = nb * samples * bands * 4
+        d2h = sum(nb * samples * (8 + (1 if r.eigcount else 0)) for r in reqs)
+        e2e = {"value": nb * samples / e2e_s / 1e6, "unit": "Mpixel/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_s * 1e3,
+               "path": "hsad_pipeline_host (C-ABI): pinned host cube -> H2D -> reduce -> fused "
+                       "detectors -> D2H" + (f" (rank 0 strip, {nb} rows)" if world > 1 else "")}
+
+    if rank != 0:
+        return
+    total_px = lines * samples
+    value = total_px / (ms_step / 1e3) / 1e6
+    peak, peak_src = hbm_peak()
+    bpp = bytes_per_pixel(bands)
+    red_ms = statistics.median(kern_ms["reduce"])
+    det_ms = statistics.median(kern_ms["detect"])
+    local_px = (r1 - r0) * samples
+    red_gbs = nb * samples * (bands * 4 + 32) / (red_ms / 1e3) / 1e9
+    step_gbs = value * 1e6 * bpp / 1e9
+    line = {
+        "metric": "Mpixels/sec for DWT+LRX/DWRX/DWEST scoring",
+        "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_config(args, cfg), parallelism=f"row-strips x{world}",
+                       row_quantum=q, strip_rows=per),
+        "roofline": {
+            "bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
+            "frac": step_gbs / peak, "traffic": None,
+            "basis": f"whole step, algorithmic {bpp} B/px (4L fp32 read + 3 fp64 maps + int8 "
+                     f"count) x px/s, {peak_src}",
+            "kernels": {
+                "reduce (K1, HBM-bound)": {"ms": red_ms, "achieved_gbs": red_gbs,
+                                           "frac": red_gbs / peak,
+                                           "bytes": "fp32 cube read + fp64 reduced write"},
+                "detect (K2-K4 fused, fp64-compute-bound)": {"ms": det_ms,
+                                                             "share": det_ms / (red_ms + det_ms),
+                                                             "px_per_s": local_px / (det_ms / 1e3)},
+            },
+        },
+        "clocks": clk,
+        "gpu_launches": 2 * args.steps,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline and host_cube is not None:
+        line["cpu_baseline"] = cpu_baseline(host_cube.numpy(), lines, nb, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

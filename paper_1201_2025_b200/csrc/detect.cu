@@ -70,7 +70,8 @@ struct DetectParams {
 template <int L>
 struct Dim {
     static constexpr int NC = L + L * (L + 1) / 2;  // moment channels
-    static constexpr int NCP = NC | 1;              // odd smem stride: conflict-free LDS.64
+    static constexpr int NC2 = (NC + 1) / 2;        // channel pairs
+    static constexpr int S2 = NC2 | 1;              // odd double2 stride: conflict-free LDS.128
 };
 
 __device__ __forceinline__ void report(const DetectParams& P, int64_t row, int64_t col, int code) {
@@ -80,28 +81,38 @@ __device__ __forceinline__ void report(const DetectParams& P, int64_t row, int64
     atomicMin(P.status, packed);
 }
 
+// Reflection on int32 coordinates with the in-range case first (detect.cpp:71-76).
+__device__ __forceinline__ int mirror32(int i, int n) {
+    if (static_cast<unsigned>(i) < static_cast<unsigned>(n)) return i;
+    if (n == 1) return 0;
+    const int period = 2 * (n - 1);
+    i = abs(i) % period;
+    return i < n ? i : period - i;
+}
+
+// y = spectrum at (global row vrow, this thread's data column) as fp64
 template <int L>
-__device__ __forceinline__ void load_pixel(const DetectParams& P, int64_t vrow, int64_t dcol,
-                                           double (&y)[L]) {
-    const int64_t drow = mirror_index(vrow, P.lines) - P.buf_row0;
-    const int64_t idx = (drow * P.samples + dcol) * L;
+__device__ __forceinline__ void load_row(const DetectParams& P, const char* colbase,
+                                         int64_t row_bytes, int vrow, double (&y)[L]) {
+    const int drow = mirror32(vrow, static_cast<int>(P.lines)) - static_cast<int>(P.buf_row0);
+    const char* p = colbase + static_cast<int64_t>(drow) * row_bytes;
     if (P.elem_bytes == 8) {
-        const double* p = static_cast<const double*>(P.cube) + idx;
+        const double* d = reinterpret_cast<const double*>(p);
         if constexpr (L % 2 == 0) {
 #pragma unroll
             for (int i = 0; i < L; i += 2) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(p + i));
+                const double2 v = __ldg(reinterpret_cast<const double2*>(d + i));
                 y[i] = v.x;
                 y[i + 1] = v.y;
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < L; ++i) y[i] = __ldg(p + i);
+            for (int i = 0; i < L; ++i) y[i] = __ldg(d + i);
         }
     } else {
-        const float* p = static_cast<const float*>(P.cube) + idx;
+        const float* f = reinterpret_cast<const float*>(p);
 #pragma unroll
-        for (int i = 0; i < L; ++i) y[i] = static_cast<double>(__ldg(p + i));
+        for (int i = 0; i < L; ++i) y[i] = static_cast<double>(__ldg(f + i));
     }
 }
 
@@ -235,21 +246,50 @@ __device__ __forceinline__ void rotate(T (&a)[L][L], T (&v)[L][L], int p, int q,
 // tan of the Jacobi angle for the pair (p, q): t = sgn(th)/(|th| + sqrt(th^2 + 1)),
 // th = (a_qq - a_pp) / (2 a_pq); for |a_pq| << |a_qq - a_pp| the series
 // t = x (1 - x^2), x = a_pq / (a_qq - a_pp), is exact to fp64 when |x| < 1e-4.
+// Both are branch-free (selects only) so a round's two independent rotations
+// can be scheduled together; a_pq == 0 gives t = 0 (identity rotation).
 __device__ __forceinline__ float jacobi_t(float app, float aqq, float apq) {
-    const float th = 0.5f * (aqq - app) / apq;
-    const float t = 1.0f / (fabsf(th) + sqrtf(fmaf(th, th, 1.0f)));
-    return th < 0.0f ? -t : t;
+    const float th = 0.5f * __fdividef(aqq - app, apq);
+    const float ath = fabsf(th);
+    const float r = fmaf(th, th, 1.0f);
+    // MUFU-only: sqrt(r) = r * rsqrt(r); for |th| huge t -> 1/(2|th|)
+    float t = ath > 1e15f ? __fdividef(0.5f, ath) : __fdividef(1.0f, ath + r * rsqrtf(r));
+    t = th < 0.0f ? -t : t;
+    return apq == 0.0f ? 0.0f : t;
 }
 __device__ __forceinline__ double jacobi_t(double app, double aqq, double apq) {
     const double h = aqq - app;
-    if (fabs(apq) < 1e-4 * fabs(h)) {
-        const double x = apq * fast_rcp(h);
-        return x * fma(-x, x, 1.0);
-    }
+    const double x = apq * fast_rcp(h);
+    const double t_small = x * fma(-x, x, 1.0);
     const double th = 0.5 * h * fast_rcp(apq);
     const double r = fma(th, th, 1.0);
-    const double t = fast_rcp(fabs(th) + r * rsqrt(r));
-    return th < 0.0 ? -t : t;
+    double t = fast_rcp(fabs(th) + r * rsqrt(r));
+    t = th < 0.0 ? -t : t;
+    t = fabs(apq) < 1e-4 * fabs(h) ? t_small : t;
+    return apq == 0.0 ? 0.0 : t;
+}
+
+// One Jacobi sweep. For L = 4 the pairs go in parallel order — rounds of two
+// disjoint rotations {(0,1),(2,3)}, {(0,2),(1,3)}, {(0,3),(1,2)} — whose angles
+// are independent, doubling the instruction-level parallelism of the chain.
+template <int L, typename T>
+__device__ __forceinline__ void jacobi_sweep(T (&a)[L][L], T (&v)[L][L]) {
+    if constexpr (L == 4) {
+        constexpr int pp[6] = {0, 2, 0, 1, 0, 1};
+        constexpr int qq[6] = {1, 3, 2, 3, 3, 2};
+#pragma unroll
+        for (int r = 0; r < 6; r += 2) {
+            const T t0 = jacobi_t(a[pp[r]][pp[r]], a[qq[r]][qq[r]], a[pp[r]][qq[r]]);
+            const T t1 = jacobi_t(a[pp[r + 1]][pp[r + 1]], a[qq[r + 1]][qq[r + 1]], a[pp[r + 1]][qq[r + 1]]);
+            rotate<L, T>(a, v, pp[r], qq[r], t0);
+            rotate<L, T>(a, v, pp[r + 1], qq[r + 1], t1);
+        }
+    } else {
+#pragma unroll
+        for (int p = 0; p < L - 1; ++p)
+#pragma unroll
+            for (int q = p + 1; q < L; ++q) rotate<L, T>(a, v, p, q, jacobi_t(a[p][p], a[q][q], a[p][q]));
+    }
 }
 
 // symmetric_eigen (stats.cpp:64-89) for the small DWEST matrix.
@@ -278,13 +318,7 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
             v32[i][j] = i == j ? 1.0f : 0.0f;
         }
 #pragma unroll 1
-    for (int sweep = 0; sweep < 4; ++sweep) {
-#pragma unroll
-        for (int p = 0; p < L - 1; ++p)
-#pragma unroll
-            for (int q = p + 1; q < L; ++q)
-                if (a32[p][q] != 0.0f) rotate<L, float>(a32, v32, p, q, jacobi_t(a32[p][p], a32[q][q], a32[p][q]));
-    }
+    for (int sweep = 0; sweep < 4; ++sweep) jacobi_sweep<L, float>(a32, v32);
     // modified Gram-Schmidt in fp64
 #pragma unroll
     for (int j = 0; j < L; ++j) {
@@ -327,13 +361,7 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
             B[j][i] = acc;
         }
 #pragma unroll 1
-    for (int sweep = 0; sweep < 2; ++sweep) {
-#pragma unroll
-        for (int p = 0; p < L - 1; ++p)
-#pragma unroll
-            for (int q = p + 1; q < L; ++q)
-                if (B[p][q] != 0.0) rotate<L, double>(B, V, p, q, jacobi_t(B[p][p], B[q][q], B[p][q]));
-    }
+    for (int sweep = 0; sweep < 2; ++sweep) jacobi_sweep<L, double>(B, V);
 #pragma unroll
     for (int i = 0; i < L; ++i) w[i] = B[i][i];
 #pragma unroll
@@ -378,13 +406,16 @@ __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s
 template <int L, int NBOX>
 __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
     constexpr int NC = Dim<L>::NC;
-    constexpr int NCP = Dim<L>::NCP;
-    extern __shared__ double s_v[];  // [NT][NCP]
+    constexpr int NC2 = Dim<L>::NC2;
+    constexpr int S2 = Dim<L>::S2;
+    extern __shared__ double2 s_v2[];  // [NT][S2] channel pairs
 
     const int t = threadIdx.x;
     const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P.tw;
     const int64_t vcol = c0 - P.rmax + t;
-    const int64_t dcol = mirror_index(vcol, P.samples);
+    const int64_t dcol = mirror32(static_cast<int>(vcol), static_cast<int>(P.samples));
+    const int64_t row_bytes = P.samples * L * P.elem_bytes;
+    const char* colbase = static_cast<const char*>(P.cube) + dcol * L * P.elem_bytes;
     const int64_t ra = P.row_begin + static_cast<int64_t>(blockIdx.y) * P.chunk;
     const int64_t rb = min(ra + P.chunk, P.row_end);
     if (ra >= rb) return;
@@ -394,59 +425,98 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
     double shift[L];
     {
         double y[L];
-        load_pixel<L>(P, ra, c0, y);
+        load_row<L>(P, static_cast<const char*>(P.cube) + c0 * L * P.elem_bytes, row_bytes,
+                    static_cast<int>(ra), y);
 #pragma unroll
         for (int i = 0; i < L; ++i) shift[i] = y[i];
     }
     auto shifted = [&](int64_t vrow, double (&y)[L]) {
-        load_pixel<L>(P, vrow, dcol, y);
+        load_row<L>(P, colbase, row_bytes, static_cast<int>(vrow), y);
 #pragma unroll
         for (int i = 0; i < L; ++i) y[i] -= shift[i];
     };
 
-    double V[NBOX][NC];
+    // Vertical window sums of this thread's column live in shared memory:
+    // s_v2[(k*NT + t)*S2 + pair]. Each thread updates only its own slot; the
+    // horizontal pass then reads its 2R+1 neighbours in place.
+    const int NT = blockDim.x;
+    int kmax = 0;
+#pragma unroll
+    for (int k = 1; k < NBOX; ++k)
+        if (P.radius[k] > P.radius[kmax]) kmax = k;
+    const int Rmax = P.radius[kmax];
 #pragma unroll
     for (int k = 0; k < NBOX; ++k) {
+        double v[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) V[k][c] = 0.0;
+        for (int c = 0; c < NC; ++c) v[c] = 0.0;
         const int R = P.radius[k];
         for (int d = -R; d <= R; ++d) {
             double y[L];
             shifted(ra + d, y);
-            add_moments<L>(V[k], y, 1.0);
+            add_moments<L>(v, y, 1.0);
         }
+        double2* dst = s_v2 + (k * NT + t) * S2;
+#pragma unroll
+        for (int c2 = 0; c2 < NC2; ++c2)
+            dst[c2] = make_double2(v[2 * c2], 2 * c2 + 1 < NC ? v[2 * c2 + 1] : 0.0);
     }
+    // the largest box's entering row is the only cold global load per step:
+    // fetch it one step ahead
+    double ynext[L];
+    shifted(ra + 1 + Rmax, ynext);
 
     for (int64_t r = ra; r < rb; ++r) {
         if (r > ra) {
+            double yin_max[L];
+#pragma unroll
+            for (int i = 0; i < L; ++i) yin_max[i] = ynext[i];
+            if (r + 1 < rb) shifted(r + 1 + Rmax, ynext);
 #pragma unroll
             for (int k = 0; k < NBOX; ++k) {
                 const int R = P.radius[k];
-                double yin[L], yout[L];
-                shifted(r + R, yin);
+                double yin[L], yout[L], dm[NC];
+                if (k == kmax) {
+#pragma unroll
+                    for (int i = 0; i < L; ++i) yin[i] = yin_max[i];
+                } else {
+                    shifted(r + R, yin);
+                }
                 shifted(r - 1 - R, yout);
-                add_moments<L>(V[k], yin, 1.0);
-                add_moments<L>(V[k], yout, -1.0);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) dm[c] = 0.0;
+                add_moments<L>(dm, yin, 1.0);
+                add_moments<L>(dm, yout, -1.0);
+                double2* dst = s_v2 + (k * NT + t) * S2;
+#pragma unroll
+                for (int c2 = 0; c2 < NC2; ++c2) {
+                    double2 v = dst[c2];
+                    v.x += dm[2 * c2];
+                    if (2 * c2 + 1 < NC) v.y += dm[2 * c2 + 1];
+                    dst[c2] = v;
+                }
             }
         }
+        __syncthreads();
         double S[NBOX][NC];
 #pragma unroll
         for (int k = 0; k < NBOX; ++k) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) s_v[t * NCP + c] = V[k][c];
-            __syncthreads();
 #pragma unroll
             for (int c = 0; c < NC; ++c) S[k][c] = 0.0;
             if (out_col) {
                 const int R = P.radius[k];
                 for (int d = -R; d <= R; ++d) {
-                    const double* src = s_v + (t + d) * NCP;
+                    const double2* src = s_v2 + (k * NT + t + d) * S2;
 #pragma unroll
-                    for (int c = 0; c < NC; ++c) S[k][c] += src[c];
+                    for (int c2 = 0; c2 < NC2; ++c2) {
+                        const double2 v = src[c2];
+                        S[k][2 * c2] += v.x;
+                        if (2 * c2 + 1 < NC) S[k][2 * c2 + 1] += v.y;
+                    }
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();
         if (!out_col) continue;
 
         const int64_t col = vcol;
@@ -581,7 +651,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
 
 template <int L>
 cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(nt) * Dim<L>::NCP * sizeof(double);
+    const size_t smem = static_cast<size_t>(P.nbox) * nt * Dim<L>::S2 * sizeof(double2);
     switch (P.nbox) {
 #define HSAD_DK(NB)                                                                   \
     case NB: {                                                                        \
