@@ -403,23 +403,169 @@ __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s
     else static_cast<float*>(R.scores)[o] = static_cast<float>(s);
 }
 
+// Per-pixel solves of every request from the box sums S (detect.cpp:168-271).
 template <int L, int NBOX>
-__global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
+__device__ __forceinline__ void solve_pixel(const DetectParams& P, const double (&S)[NBOX][Dim<L>::NC],
+                                            const double (&yc)[L], int64_t r, int64_t col) {
+    constexpr int NC = Dim<L>::NC;
+    const int64_t o = (r - P.row_begin) * P.samples + col;
+    const int64_t lin = r * P.samples + col;
+        for (int q = 0; q < P.nreq; ++q) {
+        // static indices only: a dynamic P.req[q] spills the param array to the stack
+        ReqDev R = P.req[0];
+#pragma unroll
+        for (int qq = 1; qq < kMaxRequests; ++qq)
+            if (q == qq) R = P.req[qq];
+        if (R.algo == HSAD_LRX) {
+            // detect.cpp:168-188: background = box - centre (or - guard box)
+            double bg[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
+#pragma unroll
+            for (int k = 0; k < NBOX; ++k)
+                if (k == R.box_a) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) bg[c] = S[k][c];
+                }
+            if (R.box_b < 0) {
+                add_moments<L>(bg, yc, -1.0);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NBOX; ++k)
+                    if (k == R.box_b) {
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) bg[c] -= S[k][c];
+                    }
+            }
+            double mu[L], cm[L][L], dv[L];
+            mean_cov<L>(bg, R.n_a, mu, cm);
+            double dmax = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+                dv[i] = yc[i] - mu[i];
+                dmax = fmax(dmax, fabs(dv[i]));
+            }
+            double score = 0.0;
+            if (dmax > 0.0) {
+                double delta = 0.0;
+                const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
+                if (lin == P.diag_lin) *P.diag_out = delta;
+                if (code) {
+                    report(P, r, col, code);
+                    score = 0.0;
+                }
+            }
+            store_score(R, o, fmax(score, 0.0));
+        } else {
+            double sin_[NC], sann[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                sin_[c] = 0.0;
+                sann[c] = 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < NBOX; ++k) {
+                if (k == R.box_b) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) sin_[c] = S[k][c];
+                }
+                if (k == R.box_a) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) sann[c] = S[k][c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) sann[c] -= sin_[c];
+            double mu_in[L], mu_out[L], c_out[L][L], md[L];
+            double c_in[L][L];
+            mean_cov<L>(sin_, R.n_a, mu_in, c_in);
+            mean_cov<L>(sann, R.n_b, mu_out, c_out);
+            double mmax = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+                md[i] = mu_in[i] - mu_out[i];
+                mmax = fmax(mmax, fabs(md[i]));
+            }
+            if (R.algo == HSAD_DWRX) {
+                // detect.cpp:204-223
+                double score = 0.0;
+                if (mmax > 0.0) {
+                    double delta = 0.0;
+                    const int code = chol_quad<L>(c_out, md, R.ridge, score, delta);
+                    if (lin == P.diag_lin) *P.diag_out = delta;
+                    if (code) {
+                        report(P, r, col, code);
+                        score = 0.0;
+                    }
+                }
+                store_score(R, o, fabs(score));
+            } else {
+                // detect.cpp:242-271
+                double cd[L][L], vec[L][L], w[L];
+#pragma unroll
+                for (int i = 0; i < L; ++i)
+#pragma unroll
+                    for (int j = 0; j < L; ++j) cd[i][j] = c_in[i][j] - c_out[i][j];
+                dwest_eigen<L>(cd, vec, w);
+                double score = 0.0;
+                int count = 0;
+                const double lmax = w[0];
+                if (lmax > 0.0) {
+                    double proj = 0.0;
+                    bool go = true;
+#pragma unroll
+                    for (int i = 0; i < L; ++i) {
+                        go = go && !(w[i] <= 0.0 || w[i] < R.frac * lmax);
+                        if (go) {
+                            double dot = 0.0;
+#pragma unroll
+                            for (int k = 0; k < L; ++k) dot = fma(vec[k][i], md[k], dot);
+                            proj += dot;
+                            ++count;
+                        }
+                    }
+                    score = fabs(proj);
+                }
+                store_score(R, o, score);
+                if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
+            }
+        }
+    }
+}
+
+// Column-strip streaming kernel. A CTA of NT threads owns TW = NT*K output columns
+// (thread t: strip columns [tK, tK+K)) plus rmax halo columns on each side, and
+// walks down a chunk of output rows:
+//   1. vertical window sums of every strip column (+halo) for every box live in
+//      shared memory; each step, thread t updates columns t, t+NT, ... with the
+//      entering row minus the leaving row (fp64 moments of shifted spectra);
+//   2. barrier; thread t slides a horizontal running sum over its K columns
+//      (2R+1 terms once, then +1/-1 per column), so each output costs O(1) per
+//      box instead of O(R); at each of its columns it solves LRX/DWRX/DWEST;
+//   3. barrier before the next row's update.
+// Smem column stride: S2 double2 per column plus one pad pair after every K
+// columns, so the per-thread segments (stride K columns) hit distinct banks.
+template <int L, int NBOX, int K>
+__global__ void __launch_bounds__(128) detect_kernel(const DetectParams P) {
     constexpr int NC = Dim<L>::NC;
     constexpr int NC2 = Dim<L>::NC2;
     constexpr int S2 = Dim<L>::S2;
-    extern __shared__ double2 s_v2[];  // [NT][S2] channel pairs
+    extern __shared__ double2 s_v2[];
 
     const int t = threadIdx.x;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P.tw;
-    const int64_t vcol = c0 - P.rmax + t;
-    const int64_t dcol = mirror32(static_cast<int>(vcol), static_cast<int>(P.samples));
-    const int64_t row_bytes = P.samples * L * P.elem_bytes;
-    const char* colbase = static_cast<const char*>(P.cube) + dcol * L * P.elem_bytes;
+    const int NT = blockDim.x;
+    const int ncol = P.tw + 2 * P.rmax;            // strip columns incl. halo
+    // pairs per box: S2 (odd) per column + one pad pair per K columns when K > 1,
+    // so a thread-to-thread stride of K*S2 + 1 pairs stays odd (conflict-free LDS.128)
+    const int box_stride = ncol * S2 + (K > 1 ? ncol / K + 1 : 0);
+    auto vslot = [&](int k, int c) -> double2* {    // c: strip column index 0..ncol-1
+        return s_v2 + k * box_stride + c * S2 + (K > 1 ? c / K : 0);
+    };
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P.tw;  // first output column
     const int64_t ra = P.row_begin + static_cast<int64_t>(blockIdx.y) * P.chunk;
     const int64_t rb = min(ra + P.chunk, P.row_end);
     if (ra >= rb) return;
-    const bool out_col = t >= P.rmax && t < P.rmax + P.tw && vcol < P.samples;
+    const int64_t row_bytes = P.samples * L * P.elem_bytes;
 
     // tile-anchored shift: the spectrum at (ra, c0)
     double shift[L];
@@ -430,83 +576,75 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
 #pragma unroll
         for (int i = 0; i < L; ++i) shift[i] = y[i];
     }
-    auto shifted = [&](int64_t vrow, double (&y)[L]) {
-        load_row<L>(P, colbase, row_bytes, static_cast<int>(vrow), y);
+    auto colbase_of = [&](int c) -> const char* {  // strip column -> data column base
+        const int64_t vcol = c0 - P.rmax + c;
+        const int dcol = mirror32(static_cast<int>(vcol), static_cast<int>(P.samples));
+        return static_cast<const char*>(P.cube) + static_cast<int64_t>(dcol) * L * P.elem_bytes;
+    };
+    auto shifted = [&](const char* cb, int64_t vrow, double (&y)[L]) {
+        load_row<L>(P, cb, row_bytes, static_cast<int>(vrow), y);
 #pragma unroll
         for (int i = 0; i < L; ++i) y[i] -= shift[i];
     };
 
-    // Vertical window sums of this thread's column live in shared memory:
-    // s_v2[(k*NT + t)*S2 + pair]. Each thread updates only its own slot; the
-    // horizontal pass then reads its 2R+1 neighbours in place.
-    const int NT = blockDim.x;
-    int kmax = 0;
+    // initial vertical sums over rows [ra - R_k, ra + R_k]
+    for (int c = t; c < ncol; c += NT) {
+        const char* cb = colbase_of(c);
 #pragma unroll
-    for (int k = 1; k < NBOX; ++k)
-        if (P.radius[k] > P.radius[kmax]) kmax = k;
-    const int Rmax = P.radius[kmax];
+        for (int k = 0; k < NBOX; ++k) {
+            double v[NC];
 #pragma unroll
-    for (int k = 0; k < NBOX; ++k) {
-        double v[NC];
+            for (int i = 0; i < NC; ++i) v[i] = 0.0;
+            const int R = P.radius[k];
+            for (int d = -R; d <= R; ++d) {
+                double y[L];
+                shifted(cb, ra + d, y);
+                add_moments<L>(v, y, 1.0);
+            }
+            double2* dst = vslot(k, c);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) v[c] = 0.0;
-        const int R = P.radius[k];
-        for (int d = -R; d <= R; ++d) {
-            double y[L];
-            shifted(ra + d, y);
-            add_moments<L>(v, y, 1.0);
+            for (int c2 = 0; c2 < NC2; ++c2)
+                dst[c2] = make_double2(v[2 * c2], 2 * c2 + 1 < NC ? v[2 * c2 + 1] : 0.0);
         }
-        double2* dst = s_v2 + (k * NT + t) * S2;
-#pragma unroll
-        for (int c2 = 0; c2 < NC2; ++c2)
-            dst[c2] = make_double2(v[2 * c2], 2 * c2 + 1 < NC ? v[2 * c2 + 1] : 0.0);
     }
-    // the largest box's entering row is the only cold global load per step:
-    // fetch it one step ahead
-    double ynext[L];
-    shifted(ra + 1 + Rmax, ynext);
 
+    const int seg0 = t * K;  // first output strip column of this thread (relative to rmax)
     for (int64_t r = ra; r < rb; ++r) {
         if (r > ra) {
-            double yin_max[L];
+            for (int c = t; c < ncol; c += NT) {
+                const char* cb = colbase_of(c);
 #pragma unroll
-            for (int i = 0; i < L; ++i) yin_max[i] = ynext[i];
-            if (r + 1 < rb) shifted(r + 1 + Rmax, ynext);
+                for (int k = 0; k < NBOX; ++k) {
+                    const int R = P.radius[k];
+                    double yin[L], yout[L], dm[NC];
+                    shifted(cb, r + R, yin);
+                    shifted(cb, r - 1 - R, yout);
 #pragma unroll
-            for (int k = 0; k < NBOX; ++k) {
-                const int R = P.radius[k];
-                double yin[L], yout[L], dm[NC];
-                if (k == kmax) {
+                    for (int i = 0; i < NC; ++i) dm[i] = 0.0;
+                    add_moments<L>(dm, yin, 1.0);
+                    add_moments<L>(dm, yout, -1.0);
+                    double2* dst = vslot(k, c);
 #pragma unroll
-                    for (int i = 0; i < L; ++i) yin[i] = yin_max[i];
-                } else {
-                    shifted(r + R, yin);
-                }
-                shifted(r - 1 - R, yout);
-#pragma unroll
-                for (int c = 0; c < NC; ++c) dm[c] = 0.0;
-                add_moments<L>(dm, yin, 1.0);
-                add_moments<L>(dm, yout, -1.0);
-                double2* dst = s_v2 + (k * NT + t) * S2;
-#pragma unroll
-                for (int c2 = 0; c2 < NC2; ++c2) {
-                    double2 v = dst[c2];
-                    v.x += dm[2 * c2];
-                    if (2 * c2 + 1 < NC) v.y += dm[2 * c2 + 1];
-                    dst[c2] = v;
+                    for (int c2 = 0; c2 < NC2; ++c2) {
+                        double2 v = dst[c2];
+                        v.x += dm[2 * c2];
+                        if (2 * c2 + 1 < NC) v.y += dm[2 * c2 + 1];
+                        dst[c2] = v;
+                    }
                 }
             }
         }
         __syncthreads();
-        double S[NBOX][NC];
+        if (seg0 < P.tw && c0 + seg0 < P.samples) {
+            double S[NBOX][NC];
+            // horizontal window of the first column of the segment
 #pragma unroll
-        for (int k = 0; k < NBOX; ++k) {
+            for (int k = 0; k < NBOX; ++k) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) S[k][c] = 0.0;
-            if (out_col) {
+                for (int i = 0; i < NC; ++i) S[k][i] = 0.0;
                 const int R = P.radius[k];
                 for (int d = -R; d <= R; ++d) {
-                    const double2* src = s_v2 + (k * NT + t + d) * S2;
+                    const double2* src = vslot(k, P.rmax + seg0 + d);
 #pragma unroll
                     for (int c2 = 0; c2 < NC2; ++c2) {
                         const double2 v = src[c2];
@@ -515,172 +653,77 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams P) {
                     }
                 }
             }
-        }
-        __syncthreads();
-        if (!out_col) continue;
-
-        const int64_t col = vcol;
-        const int64_t o = (r - P.row_begin) * P.samples + col;
-        const int64_t lin = r * P.samples + col;
-        double yc[L];
-        shifted(r, yc);
-
-        for (int q = 0; q < P.nreq; ++q) {
-            // static indices only: a dynamic P.req[q] spills the param array to the stack
-            ReqDev R = P.req[0];
+#pragma unroll 1
+            for (int j = 0; j < K; ++j) {
+                const int sc = seg0 + j;
+                const int64_t col = c0 + sc;
+                if (sc >= P.tw || col >= P.samples) break;
+                if (j > 0) {
 #pragma unroll
-            for (int qq = 1; qq < kMaxRequests; ++qq)
-                if (q == qq) R = P.req[qq];
-            if (R.algo == HSAD_LRX) {
-                // detect.cpp:168-188: background = box - centre (or - guard box)
-                double bg[NC];
+                    for (int k = 0; k < NBOX; ++k) {
+                        const int R = P.radius[k];
+                        const double2* in = vslot(k, P.rmax + sc + R);
+                        const double2* out = vslot(k, P.rmax + sc - 1 - R);
 #pragma unroll
-                for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
-#pragma unroll
-                for (int k = 0; k < NBOX; ++k)
-                    if (k == R.box_a) {
-#pragma unroll
-                        for (int c = 0; c < NC; ++c) bg[c] = S[k][c];
-                    }
-                if (R.box_b < 0) {
-                    add_moments<L>(bg, yc, -1.0);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < NBOX; ++k)
-                        if (k == R.box_b) {
-#pragma unroll
-                            for (int c = 0; c < NC; ++c) bg[c] -= S[k][c];
-                        }
-                }
-                double mu[L], cm[L][L], dv[L];
-                mean_cov<L>(bg, R.n_a, mu, cm);
-                double dmax = 0.0;
-#pragma unroll
-                for (int i = 0; i < L; ++i) {
-                    dv[i] = yc[i] - mu[i];
-                    dmax = fmax(dmax, fabs(dv[i]));
-                }
-                double score = 0.0;
-                if (dmax > 0.0) {
-                    double delta = 0.0;
-                    const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
-                    if (lin == P.diag_lin) *P.diag_out = delta;
-                    if (code) {
-                        report(P, r, col, code);
-                        score = 0.0;
-                    }
-                }
-                store_score(R, o, fmax(score, 0.0));
-            } else {
-                double sin_[NC], sann[NC];
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    sin_[c] = 0.0;
-                    sann[c] = 0.0;
-                }
-#pragma unroll
-                for (int k = 0; k < NBOX; ++k) {
-                    if (k == R.box_b) {
-#pragma unroll
-                        for (int c = 0; c < NC; ++c) sin_[c] = S[k][c];
-                    }
-                    if (k == R.box_a) {
-#pragma unroll
-                        for (int c = 0; c < NC; ++c) sann[c] = S[k][c];
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < NC; ++c) sann[c] -= sin_[c];
-                double mu_in[L], mu_out[L], c_out[L][L], md[L];
-                double c_in[L][L];
-                mean_cov<L>(sin_, R.n_a, mu_in, c_in);
-                mean_cov<L>(sann, R.n_b, mu_out, c_out);
-                double mmax = 0.0;
-#pragma unroll
-                for (int i = 0; i < L; ++i) {
-                    md[i] = mu_in[i] - mu_out[i];
-                    mmax = fmax(mmax, fabs(md[i]));
-                }
-                if (R.algo == HSAD_DWRX) {
-                    // detect.cpp:204-223
-                    double score = 0.0;
-                    if (mmax > 0.0) {
-                        double delta = 0.0;
-                        const int code = chol_quad<L>(c_out, md, R.ridge, score, delta);
-                        if (lin == P.diag_lin) *P.diag_out = delta;
-                        if (code) {
-                            report(P, r, col, code);
-                            score = 0.0;
+                        for (int c2 = 0; c2 < NC2; ++c2) {
+                            const double2 a = in[c2], b = out[c2];
+                            S[k][2 * c2] += a.x - b.x;
+                            if (2 * c2 + 1 < NC) S[k][2 * c2 + 1] += a.y - b.y;
                         }
                     }
-                    store_score(R, o, fabs(score));
-                } else {
-                    // detect.cpp:242-271
-                    double cd[L][L], vec[L][L], w[L];
-#pragma unroll
-                    for (int i = 0; i < L; ++i)
-#pragma unroll
-                        for (int j = 0; j < L; ++j) cd[i][j] = c_in[i][j] - c_out[i][j];
-                    dwest_eigen<L>(cd, vec, w);
-                    double score = 0.0;
-                    int count = 0;
-                    const double lmax = w[0];
-                    if (lmax > 0.0) {
-                        double proj = 0.0;
-                        bool go = true;
-#pragma unroll
-                        for (int i = 0; i < L; ++i) {
-                            go = go && !(w[i] <= 0.0 || w[i] < R.frac * lmax);
-                            if (go) {
-                                double dot = 0.0;
-#pragma unroll
-                                for (int k = 0; k < L; ++k) dot = fma(vec[k][i], md[k], dot);
-                                proj += dot;
-                                ++count;
-                            }
-                        }
-                        score = fabs(proj);
-                    }
-                    store_score(R, o, score);
-                    if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
                 }
+                double yc[L];
+                shifted(colbase_of(P.rmax + sc), r, yc);
+                solve_pixel<L, NBOX>(P, S, yc, r, col);
             }
         }
+        __syncthreads();
     }
 }
 
-template <int L>
-cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(P.nbox) * nt * Dim<L>::S2 * sizeof(double2);
-    switch (P.nbox) {
-#define HSAD_DK(NB)                                                                   \
-    case NB: {                                                                        \
-        auto k = detect_kernel<L, NB>;                                                \
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                             static_cast<int>(smem));                 \
-        if (e != cudaSuccess) return e;                                               \
-        k<<<grid, nt, smem, s>>>(P);                                                  \
-        return cudaGetLastError();                                                    \
+template <int L, int NB>
+cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
+    const int ncol = P.tw + 2 * P.rmax;
+    auto go = [&](auto kern, int K) -> cudaError_t {
+        const size_t smem = static_cast<size_t>(NB) *
+                            (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)) * sizeof(double2);
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, nt, smem, s>>>(P);
+        return cudaGetLastError();
+    };
+    if constexpr (L == 4) {  // multi-column segments only on the 4-band (DWT) hot path
+        if (kcols == 4) return go(detect_kernel<L, NB, 4>, 4);
+        if (kcols == 2) return go(detect_kernel<L, NB, 2>, 2);
     }
-        HSAD_DK(1)
-        HSAD_DK(2)
-        HSAD_DK(3)
-        HSAD_DK(4)
-#undef HSAD_DK
+    if (kcols == 1) return go(detect_kernel<L, NB, 1>, 1);
+    return cudaErrorInvalidValue;
+}
+
+template <int L>
+cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
+    switch (P.nbox) {
+        case 1: return launch_lk<L, 1>(P, grid, nt, kcols, s);
+        case 2: return launch_lk<L, 2>(P, grid, nt, kcols, s);
+        case 3: return launch_lk<L, 3>(P, grid, nt, kcols, s);
+        case 4: return launch_lk<L, 4>(P, grid, nt, kcols, s);
     }
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_detect(int bands, const DetectParams& P, dim3 grid, int nt, cudaStream_t s) {
+cudaError_t launch_detect(int bands, const DetectParams& P, dim3 grid, int nt, int kcols,
+                          cudaStream_t s) {
     switch (bands) {
-        case 1: return launch_l<1>(P, grid, nt, s);
-        case 2: return launch_l<2>(P, grid, nt, s);
-        case 3: return launch_l<3>(P, grid, nt, s);
-        case 4: return launch_l<4>(P, grid, nt, s);
-        case 5: return launch_l<5>(P, grid, nt, s);
-        case 6: return launch_l<6>(P, grid, nt, s);
-        case 7: return launch_l<7>(P, grid, nt, s);
-        case 8: return launch_l<8>(P, grid, nt, s);
+        case 1: return launch_l<1>(P, grid, nt, kcols, s);
+        case 2: return launch_l<2>(P, grid, nt, kcols, s);
+        case 3: return launch_l<3>(P, grid, nt, kcols, s);
+        case 4: return launch_l<4>(P, grid, nt, kcols, s);
+        case 5: return launch_l<5>(P, grid, nt, kcols, s);
+        case 6: return launch_l<6>(P, grid, nt, kcols, s);
+        case 7: return launch_l<7>(P, grid, nt, kcols, s);
+        case 8: return launch_l<8>(P, grid, nt, kcols, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -699,6 +742,7 @@ const char* algo_name(int a) {
 struct Plan {
     DetectParams P{};
     int nt = 128;
+    int kcols = 1;
     dim3 grid;
 };
 
@@ -778,11 +822,16 @@ hsad_status plan_requests(const hsad_detect_request* reqs, int n, Plan& plan) {
 
 }  // namespace
 
+// Output columns per thread (before the shared-memory fit check): wide images
+// amortise the horizontal window over more columns.
+int kcols_for(int64_t samples) { return samples >= 2048 ? 4 : samples >= 512 ? 2 : 1; }
+
 int64_t row_quantum(int64_t lines, int64_t samples) {
     // chunk height: large enough to amortise the 2R+1-row warm-up, small enough
     // that the grid fills the GPU twice (148 SMs); depends on the image only
     const int sms = 148;
-    const int64_t strips = (samples + 117) / 118;
+    const int64_t tw = 128 * kcols_for(samples);
+    const int64_t strips = (samples + tw - 1) / tw;
     int64_t q = 64;
     while (q > 8 && strips * ((lines + q - 1) / q) < 2 * sms) q /= 2;
     return q;
@@ -846,8 +895,23 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     P.row_begin = row_begin;
     P.row_end = row_end;
     P.chunk = row_quantum(lines, samples);
-    plan.nt = 2 * P.rmax + 32 <= 128 ? 128 : 256;
-    P.tw = plan.nt - 2 * P.rmax;
+    // 128 threads x K output columns; shrink K until the per-box vertical sums
+    // (strip + halo columns) fit comfortably in shared memory
+    plan.nt = 128;
+    int kc = bands == 4 ? kcols_for(samples) : 1;
+    auto smem_for = [&](int k) {
+        const int64_t ncol = 128 * k + 2 * P.rmax;
+        const int s2 = ((bands + bands * (bands + 1) / 2 + 1) / 2) | 1;
+        return static_cast<int64_t>(P.nbox) * (ncol * s2 + (k > 1 ? ncol / k + 1 : 0)) * 16;
+    };
+    while (kc > 1 && smem_for(kc) > 110 * 1024) kc /= 2;
+    if (smem_for(kc) > 227 * 1024)
+        return set_error(HSAD_E_UNSUPPORTED,
+                         "window statistics for " + std::to_string(P.nbox) + " window sizes up to " +
+                             std::to_string(2 * P.rmax + 1) + " at " + std::to_string(bands) +
+                             " bands exceed shared memory; split the requests");
+    plan.kcols = kc;
+    P.tw = 128 * kc;
     P.diag_lin = -1;
     P.diag_out = nullptr;
     const int64_t strips = (samples + P.tw - 1) / P.tw;
@@ -864,7 +928,7 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     }
     P.status = status;
-    cudaError_t e = launch_detect(bands, P, plan.grid, plan.nt, s);
+    cudaError_t e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
     if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
     if (!sync) return HSAD_OK;
 
@@ -900,7 +964,7 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                     D.req[q].eigcount = reinterpret_cast<int8_t*>(
                         scratch + static_cast<size_t>(samples) * (9 * q + 8));
             }
-            e = launch_detect(bands, D, dim3(plan.grid.x, 1), plan.nt, s);
+            e = launch_detect(bands, D, dim3(plan.grid.x, 1), plan.nt, plan.kcols, s);
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(&delta, d_diag, sizeof(double), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
