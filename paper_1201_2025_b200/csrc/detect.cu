@@ -214,26 +214,31 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
     return 0;
 }
 
-// One Jacobi rotation zeroing a[p][q]; tan-half-angle form (Rutishauser).
+// Symmetric L x L matrices are kept as their upper triangle only (a[i][j], i <= j);
+// sym(a, i, j) addresses element (i, j) for any order with compile-time indices,
+// so rotations never write the mirrored copy.
 template <int L, typename T>
-__device__ __forceinline__ void rotate(T (&a)[L][L], T (&v)[L][L], int p, int q, T t) {
+__device__ __forceinline__ T& sym(T (&a)[L][L], int i, int j) {
+    return i <= j ? a[i][j] : a[j][i];
+}
+
+// One Jacobi rotation zeroing (p, q) with tan t and cos c (sin = t c):
+// A <- J^T A J on the upper triangle, V <- V J.
+template <int L, typename T>
+__device__ __forceinline__ void rotate_tc(T (&a)[L][L], T (&v)[L][L], int p, int q, T t, T c) {
     const T apq = a[p][q];
-    const T c = rsqrt(T(1) + t * t);
     const T s = t * c;
     a[p][p] -= t * apq;
     a[q][q] += t * apq;
     a[p][q] = T(0);
-    a[q][p] = T(0);
 #pragma unroll
     for (int k = 0; k < L; ++k) {
         if (k == p || k == q) continue;
-        const T akp = a[k][p], akq = a[k][q];
-        const T nkp = c * akp - s * akq;
-        const T nkq = s * akp + c * akq;
-        a[k][p] = nkp;
-        a[p][k] = nkp;
-        a[k][q] = nkq;
-        a[q][k] = nkq;
+        T& akp = sym<L, T>(a, k, p);
+        T& akq = sym<L, T>(a, k, q);
+        const T x = akp, y = akq;
+        akp = c * x - s * y;
+        akq = s * x + c * y;
     }
 #pragma unroll
     for (int k = 0; k < L; ++k) {
@@ -243,82 +248,116 @@ __device__ __forceinline__ void rotate(T (&a)[L][L], T (&v)[L][L], int p, int q,
     }
 }
 
-// tan of the Jacobi angle for the pair (p, q): t = sgn(th)/(|th| + sqrt(th^2 + 1)),
-// th = (a_qq - a_pp) / (2 a_pq); for |a_pq| << |a_qq - a_pp| the series
-// t = x (1 - x^2), x = a_pq / (a_qq - a_pp), is exact to fp64 when |x| < 1e-4.
-// Both are branch-free (selects only) so a round's two independent rotations
-// can be scheduled together; a_pq == 0 gives t = 0 (identity rotation).
-__device__ __forceinline__ float jacobi_t(float app, float aqq, float apq) {
+// fp32 Jacobi angle (MUFU only): t = sgn(th)/(|th| + sqrt(th^2 + 1)),
+// th = (a_qq - a_pp)/(2 a_pq); a_pq == 0 gives the identity rotation.
+__device__ __forceinline__ float jacobi_t32(float app, float aqq, float apq) {
     const float th = 0.5f * __fdividef(aqq - app, apq);
     const float ath = fabsf(th);
     const float r = fmaf(th, th, 1.0f);
-    // MUFU-only: sqrt(r) = r * rsqrt(r); for |th| huge t -> 1/(2|th|)
     float t = ath > 1e15f ? __fdividef(0.5f, ath) : __fdividef(1.0f, ath + r * rsqrtf(r));
     t = th < 0.0f ? -t : t;
     return apq == 0.0f ? 0.0f : t;
 }
-__device__ __forceinline__ double jacobi_t(double app, double aqq, double apq) {
+
+// fp64 Jacobi angle, general case (fast rcp/rsqrt, ~1 ulp)
+__device__ __forceinline__ double jacobi_t64(double app, double aqq, double apq) {
     const double h = aqq - app;
-    const double x = apq * fast_rcp(h);
-    const double t_small = x * fma(-x, x, 1.0);
     const double th = 0.5 * h * fast_rcp(apq);
     const double r = fma(th, th, 1.0);
     double t = fast_rcp(fabs(th) + r * rsqrt(r));
     t = th < 0.0 ? -t : t;
-    t = fabs(apq) < 1e-4 * fabs(h) ? t_small : t;
     return apq == 0.0 ? 0.0 : t;
 }
 
-// One Jacobi sweep. For L = 4 the pairs go in parallel order — rounds of two
-// disjoint rotations {(0,1),(2,3)}, {(0,2),(1,3)}, {(0,3),(1,2)} — whose angles
-// are independent, doubling the instruction-level parallelism of the chain.
-template <int L, typename T>
-__device__ __forceinline__ void jacobi_sweep(T (&a)[L][L], T (&v)[L][L]) {
-    if constexpr (L == 4) {
-        constexpr int pp[6] = {0, 2, 0, 1, 0, 1};
-        constexpr int qq[6] = {1, 3, 2, 3, 3, 2};
-#pragma unroll
-        for (int r = 0; r < 6; r += 2) {
-            const T t0 = jacobi_t(a[pp[r]][pp[r]], a[qq[r]][qq[r]], a[pp[r]][qq[r]]);
-            const T t1 = jacobi_t(a[pp[r + 1]][pp[r + 1]], a[qq[r + 1]][qq[r + 1]], a[pp[r + 1]][qq[r + 1]]);
-            rotate<L, T>(a, v, pp[r], qq[r], t0);
-            rotate<L, T>(a, v, pp[r + 1], qq[r + 1], t1);
+// Pairs of one sweep; for L = 4 in parallel order (rounds of two disjoint pairs
+// {(0,1),(2,3)}, {(0,2),(1,3)}, {(0,3),(1,2)} whose angles are independent).
+template <int L>
+struct SweepOrder {
+    static constexpr int N = L * (L - 1) / 2;
+    int p[N > 0 ? N : 1], q[N > 0 ? N : 1];
+    constexpr SweepOrder() : p(), q() {
+        if constexpr (L == 4) {
+            const int pp[6] = {0, 2, 0, 1, 0, 1}, qq[6] = {1, 3, 2, 3, 3, 2};
+            for (int i = 0; i < 6; ++i) {
+                p[i] = pp[i];
+                q[i] = qq[i];
+            }
+        } else {
+            int n = 0;
+            for (int i = 0; i < L - 1; ++i)
+                for (int j = i + 1; j < L; ++j) {
+                    p[n] = i;
+                    q[n] = j;
+                    ++n;
+                }
         }
-    } else {
+    }
+};
+
+template <int L>
+__device__ __forceinline__ void sweep32(float (&a)[L][L], float (&v)[L][L]) {
+    constexpr SweepOrder<L> ord;
 #pragma unroll
-        for (int p = 0; p < L - 1; ++p)
-#pragma unroll
-            for (int q = p + 1; q < L; ++q) rotate<L, T>(a, v, p, q, jacobi_t(a[p][p], a[q][q], a[p][q]));
+    for (int i = 0; i < SweepOrder<L>::N; ++i) {
+        const int p = ord.p[i], q = ord.q[i];
+        const float t = jacobi_t32(a[p][p], a[q][q], a[p][q]);
+        rotate_tc<L, float>(a, v, p, q, t, rsqrtf(fmaf(t, t, 1.0f)));
     }
 }
 
-// symmetric_eigen (stats.cpp:64-89) for the small DWEST matrix.
-//   1. cyclic Jacobi in fp32 on the max-normalised matrix (4 sweeps): the cheap
-//      part of the work, MUFU rcp/rsqrt;
-//   2. fp64 modified Gram-Schmidt of those vectors -> exactly orthonormal Q,
-//      B = Q^T A Q in fp64 (off-diagonal ~1e-7 |A|);
-//   3. two fp64 Jacobi sweeps on B (quadratic convergence: 1e-7 -> 1e-14 -> 1e-28),
+// fp64 polish sweep on a nearly diagonal matrix. When every lane of the warp
+// has |a_pq| < 1e-4 |a_qq - a_pp| the angle comes from the series
+// t = x (1 - x^2), x = a_pq / (a_qq - a_pp), and c = 1 - t^2/2 (both exact to
+// fp64 for |x| < 1e-4); otherwise the general formula. The choice is
+// warp-uniform so the cheap path costs no divergence.
+template <int L>
+__device__ __forceinline__ void sweep64(double (&a)[L][L], double (&v)[L][L]) {
+    constexpr SweepOrder<L> ord;
+#pragma unroll
+    for (int i = 0; i < SweepOrder<L>::N; ++i) {
+        const int p = ord.p[i], q = ord.q[i];
+        const double apq = a[p][q], h = a[q][q] - a[p][p];
+        const bool small = fabs(apq) < 1e-4 * fabs(h) || apq == 0.0;
+        double t, c;
+        if (__all_sync(__activemask(), small)) {
+            const double x = apq == 0.0 ? 0.0 : apq * fast_rcp(h);
+            t = x * fma(-x, x, 1.0);
+            c = fma(-0.5 * t, t, 1.0);
+        } else {
+            t = small ? (apq == 0.0 ? 0.0 : apq * fast_rcp(h)) : jacobi_t64(a[p][p], a[q][q], apq);
+            if (small) t = t * fma(-t, t, 1.0);
+            c = rsqrt(fma(t, t, 1.0));
+        }
+        rotate_tc<L, double>(a, v, p, q, t, c);
+    }
+}
+
+// symmetric_eigen (stats.cpp:64-89) for the small DWEST matrix, unsorted:
+//   1. three parallel-order Jacobi sweeps in fp32 on the max-normalised matrix;
+//   2. fp64 modified Gram-Schmidt of those vectors -> orthonormal Q,
+//      B = Q^T A Q in fp64 (off-diagonal ~1e-6 |A|);
+//   3. two fp64 polish sweeps on B (quadratic convergence to fp64 accuracy),
 //      accumulated into Q.
-// Then descending order (stable on ties) and the sign rule: the first
-// largest-|.| component of each eigenvector is made positive.
+// Returns eigenvalues w (diagonal of B) and eigenvectors V (columns), in no
+// particular order: the DWEST selection below does not need them sorted.
 template <int L>
 __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)[L][L], double (&w)[L]) {
     double amax = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
-        for (int j = 0; j < L; ++j) amax = fmax(amax, fabs(A[i][j]));
+        for (int j = i; j < L; ++j) amax = fmax(amax, fabs(A[i][j]));
     const double scale = amax > 0.0 ? fast_rcp(amax) : 1.0;
     float a32[L][L], v32[L][L];
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
         for (int j = 0; j < L; ++j) {
-            a32[i][j] = static_cast<float>(A[i][j] * scale);
+            a32[i][j] = j >= i ? static_cast<float>(A[i][j] * scale) : 0.0f;
             v32[i][j] = i == j ? 1.0f : 0.0f;
         }
 #pragma unroll 1
-    for (int sweep = 0; sweep < 4; ++sweep) jacobi_sweep<L, float>(a32, v32);
+    for (int sweep = 0; sweep < (L <= 4 ? 3 : 6); ++sweep) sweep32<L>(a32, v32);
     // modified Gram-Schmidt in fp64
 #pragma unroll
     for (int j = 0; j < L; ++j) {
@@ -339,7 +378,7 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
 #pragma unroll
         for (int k = 0; k < L; ++k) V[k][j] *= r;
     }
-    // B = V^T A V
+    // B = V^T A V (upper triangle), A given by its upper triangle
     double AV[L][L], B[L][L];
 #pragma unroll
     for (int i = 0; i < L; ++i)
@@ -347,55 +386,40 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
         for (int j = 0; j < L; ++j) {
             double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < L; ++k) acc = fma(A[i][k], V[k][j], acc);
+            for (int k = 0; k < L; ++k) acc = fma(i <= k ? A[i][k] : A[k][i], V[k][j], acc);
             AV[i][j] = acc;
         }
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
-        for (int j = i; j < L; ++j) {
+        for (int j = 0; j < L; ++j) {
+            if (j < i) {
+                B[i][j] = 0.0;
+                continue;
+            }
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < L; ++k) acc = fma(V[k][i], AV[k][j], acc);
             B[i][j] = acc;
-            B[j][i] = acc;
         }
+    // at least two polish sweeps; more (warp-uniform) until the off-diagonal mass
+    // is below (1e-15 |B|)^2 — larger matrices leave fp32 less converged
 #pragma unroll 1
-    for (int sweep = 0; sweep < 2; ++sweep) jacobi_sweep<L, double>(B, V);
+    for (int sweep = 0; sweep < 8; ++sweep) {
+        sweep64<L>(B, V);
+        if (sweep >= 1) {
+            double off = 0.0, dia = 0.0;
 #pragma unroll
-    for (int i = 0; i < L; ++i) w[i] = B[i][i];
+            for (int i = 0; i < L; ++i) {
+                dia = fma(B[i][i], B[i][i], dia);
 #pragma unroll
-    for (int pass = 0; pass < L - 1; ++pass)
-#pragma unroll
-        for (int i = 0; i < L - 1 - pass; ++i) {
-            if (w[i + 1] > w[i]) {
-                const double tw = w[i];
-                w[i] = w[i + 1];
-                w[i + 1] = tw;
-#pragma unroll
-                for (int k = 0; k < L; ++k) {
-                    const double tv = V[k][i];
-                    V[k][i] = V[k][i + 1];
-                    V[k][i + 1] = tv;
-                }
+                for (int j = i + 1; j < L; ++j) off = fma(B[i][j], B[i][j], off);
             }
-        }
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-        double best = -1.0, val = 0.0;
-#pragma unroll
-        for (int k = 0; k < L; ++k) {
-            const double av = fabs(V[k][i]);
-            if (av > best) {
-                best = av;
-                val = V[k][i];
-            }
-        }
-        if (val < 0.0) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) V[k][i] = -V[k][i];
+            if (__all_sync(__activemask(), off <= 1e-30 * dia)) break;
         }
     }
+#pragma unroll
+    for (int i = 0; i < L; ++i) w[i] = B[i][i];
 }
 
 __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s) {
@@ -507,22 +531,33 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const double 
 #pragma unroll
                     for (int j = 0; j < L; ++j) cd[i][j] = c_in[i][j] - c_out[i][j];
                 dwest_eigen<L>(cd, vec, w);
+                // detect.cpp:255-263: with eigenvalues sorted descending the loop sums
+                // v_i . m_diff while lambda_i > 0 && lambda_i >= f lambda0 and stops at
+                // the first failure. The condition is monotone in lambda_i, so the summed
+                // set is exactly {i : lambda_i > 0, lambda_i >= f lambda0}: no sort needed.
+                // Sign rule (stats.cpp:83-85): flip v_i so that its first largest-|.|
+                // component is positive.
+                double lmax = w[0];
+#pragma unroll
+                for (int i = 1; i < L; ++i) lmax = fmax(lmax, w[i]);
                 double score = 0.0;
                 int count = 0;
-                const double lmax = w[0];
                 if (lmax > 0.0) {
+                    const double cut = R.frac * lmax;
                     double proj = 0.0;
-                    bool go = true;
 #pragma unroll
                     for (int i = 0; i < L; ++i) {
-                        go = go && !(w[i] <= 0.0 || w[i] < R.frac * lmax);
-                        if (go) {
-                            double dot = 0.0;
+                        double best = fabs(vec[0][i]), lead = vec[0][i], dot = vec[0][i] * md[0];
 #pragma unroll
-                            for (int k = 0; k < L; ++k) dot = fma(vec[k][i], md[k], dot);
-                            proj += dot;
-                            ++count;
+                        for (int k = 1; k < L; ++k) {
+                            const double av = fabs(vec[k][i]);
+                            lead = av > best ? vec[k][i] : lead;
+                            best = fmax(best, av);
+                            dot = fma(vec[k][i], md[k], dot);
                         }
+                        const bool take = w[i] > 0.0 && !(w[i] < cut);
+                        proj += take ? (lead < 0.0 ? -dot : dot) : 0.0;
+                        count += take ? 1 : 0;
                     }
                     score = fabs(proj);
                 }
