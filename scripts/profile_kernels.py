@@ -15,9 +15,11 @@ cube = generate_rows(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], 0,
 W1, W2 = hs.WindowConfig.single, hs.WindowConfig.dual
 reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwrx", W2(5, 11)),
         hs.DetectRequest("dwest", W2(5, 11), eigcount=True)]
+lrx_only = [reqs[0]]
 st = torch.full((1,), -1, dtype=torch.int64, device="cuda")
 for _ in range(3):
     red = hs.reduce_cube(cube, 2, 4)
     outs = hs.detect_multi(red, reqs, status=st)
+    hs.detect_multi(red, lrx_only, status=st)
 torch.cuda.synchronize()
 print("ok", int(st.item()))
