@@ -237,10 +237,9 @@ def run_b200(args, cfg, rank, world, local, dist):
     reqs = requests(hs)
 
     # ---- row strip of this rank (aligned to the detector row quantum) + halo
-    q = hs.row_quantum(lines, samples)
-    per = -(-lines // (world * q)) * q
-    r0, r1 = min(lines, rank * per), min(lines, (rank + 1) * per)
-    b0, nb = hs.strip_rows(lines, r0, r1, reqs)
+    from paper_1201_2025_b200.sharded import plan_strip
+    plan = plan_strip(lines, samples, world, rank, reqs)
+    q, per, r0, r1, b0, nb = plan.quantum, plan.per, plan.r0, plan.r1, plan.b0, plan.nb
     cube = generate_rows(lines, samples, bands, cfg["seed"], b0, b0 + nb, cfg["rate"], device=dev)
     red = torch.empty((nb, samples, 4), dtype=torch.float64, device=dev)
     outs = [(torch.empty((r1 - r0, samples), dtype=torch.float64, device=dev),

@@ -317,3 +317,25 @@ def test_pipeline_host_equals_device_path(orc):
 def test_cpu_tensor_rejected():
     with pytest.raises(TypeError):
         hs.reduce_cube(torch.zeros((2, 2, 8)), 2, 4)
+
+
+def test_golden_vectors_from_reference_code():
+    """The kernels against tests/golden (produced by the reference's own wavelet.cpp
+    and naive detectors, tests/golden/make_golden.py)."""
+    from pathlib import Path
+    gdir = Path(__file__).resolve().parent / "golden"
+    w = np.load(gdir / "golden_wavelet.npz")
+    for key in [k for k in w.files if k.startswith("reduce_out_")]:
+        _, _, bands, seed, order, target = key.split("_")
+        got = host(hs.reduce_cube(gpu(w[f"reduce_in_{bands}_{seed}"]), int(order), int(target)))
+        assert max_rel_diff(got, w[key]) < 1e-12
+    g = np.load(gdir / "golden_detect.npz")
+    for seed in (2024, 0xACCE3):
+        c = gpu(g[f"cube_{seed}"])
+        assert max_rel_diff(host(hs.local_rx(c, W1(5)).scores), g[f"lrx5_{seed}"]) < 1e-10
+        assert max_rel_diff(host(hs.dwrx(c, W2(3, 7)).scores), g[f"dwrx37_{seed}"]) < 1e-10
+        assert max_rel_diff(host(hs.dwest(c, W2(3, 7)).scores), g[f"dwest37_{seed}"]) < 1e-10
+    c = gpu(g["cube_99"])
+    assert max_rel_diff(host(hs.local_rx(c, W1(7)).scores), g["lrx7_99"]) < 1e-10
+    assert max_rel_diff(host(hs.dwrx(c, W2(5, 9)).scores), g["dwrx59_99"]) < 1e-10
+    assert max_rel_diff(host(hs.dwest(c, W2(5, 9), 0.3).scores), g["dwest59_99"]) < 1e-10

@@ -341,3 +341,34 @@ def test_lrx_guard_extension_equals_manual_annulus(orc):
     C += 1e-6 * np.trace(C) / 3 * np.eye(3)
     d = cube[r, c] - mu
     assert abs(got[r, c] - d @ np.linalg.solve(C, d)) < 1e-9 * max(1, got[r, c])
+
+
+# ----------------------------------------------------------------- golden fixtures
+GOLDEN = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+
+
+def test_oracle_matches_reference_golden_vectors(orc):
+    """tests/golden/*.npz were produced by the reference's own code (make_golden.py);
+    this pins the restatement even where oracle/_ref is not built."""
+    w = np.load(GOLDEN / "golden_wavelet.npz")
+    for order in range(1, 11):
+        lo, hi = orc.port.daubechies(order)
+        assert np.array_equal(lo, w[f"taps_low_{order}"]) and np.array_equal(hi, w[f"taps_high_{order}"])
+    a, d = orc.port.dwt_level([1.0, 2, 3, 4], 1)
+    assert np.array_equal(a, w["haar_1234_approx"]) and np.array_equal(d, w["haar_1234_detail"])
+    for key in [k for k in w.files if k.startswith("reduce_out_")]:
+        _, _, bands, seed, order, target = key.split("_")
+        cube = w[f"reduce_in_{bands}_{seed}"]
+        assert np.array_equal(orc.port.random_cube(5, 7, int(bands), int(seed)), cube)
+        assert np.array_equal(orc.port.reduce_cube(cube, int(order), int(target)), w[key])
+    g = np.load(GOLDEN / "golden_detect.npz")
+    for seed in (2024, 0xACCE3):
+        cube = g[f"cube_{seed}"]
+        assert np.array_equal(orc.port.random_cube(10, 10, 4, seed), cube)
+        assert max_rel_diff(orc.port.local_rx(cube, 5, 1e-6), g[f"lrx5_{seed}"]) < 1e-10
+        assert max_rel_diff(orc.port.dwrx(cube, 3, 7, 1e-6), g[f"dwrx37_{seed}"]) < 1e-10
+        assert max_rel_diff(orc.port.dwest(cube, 3, 7, 0.1)[0], g[f"dwest37_{seed}"]) < 1e-10
+    cube = g["cube_99"]
+    assert max_rel_diff(orc.port.local_rx(cube, 7, 1e-6), g["lrx7_99"]) < 1e-10
+    assert max_rel_diff(orc.port.dwrx(cube, 5, 9, 1e-6), g["dwrx59_99"]) < 1e-10
+    assert max_rel_diff(orc.port.dwest(cube, 5, 9, 0.3)[0], g["dwest59_99"]) < 1e-10

@@ -1,0 +1,114 @@
+"""Multi-rank path on CPU: world_size 2 (and 3) with the gloo backend.
+
+Each rank plans its row strip, takes only its buffer rows (strip + mirror halo) from
+the host copy, computes them — here with the CPU oracle standing in for the CUDA
+kernels, since this box has no GPU — and the maps are gathered to rank 0. Rows
+outside a rank's buffer are NaN-poisoned, so a wrong halo shows up as NaN scores.
+The gathered maps must equal the single-process oracle maps exactly.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+LINES, SAMPLES, BANDS = 37, 23, 40
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_compute(full_cube):
+    """Per-strip compute with the oracle: sees only the buffer rows of the strip."""
+    import oracle
+
+    def compute(buf, plan, requests, order, target):
+        lines = plan.lines
+        poisoned = np.full((lines,) + tuple(buf.shape[1:]), np.nan, np.float64)
+        poisoned[plan.b0: plan.b0 + plan.nb] = buf.numpy()
+        # the oracle reduces every row; rows outside the buffer stay NaN
+        red = np.full((lines, buf.shape[1], target), np.nan)
+        red[plan.b0: plan.b0 + plan.nb] = oracle.port.reduce_cube(buf.numpy(), order, target)
+        outs = []
+        for r in requests:
+            rows = (plan.r0, plan.r1)
+            if r.algorithm == "lrx":
+                s = oracle.port.local_rx(red, r.window.single_size, r.ridge, rows=rows)
+                outs.append((torch.from_numpy(s), None))
+            elif r.algorithm == "dwrx":
+                s = oracle.port.dwrx(red, r.window.inner_size, r.window.outer_size, r.ridge, rows=rows)
+                outs.append((torch.from_numpy(s), None))
+            else:
+                s, c = oracle.port.dwest(red, r.window.inner_size, r.window.outer_size,
+                                         r.eigen_fraction, rows=rows)
+                outs.append((torch.from_numpy(s), torch.from_numpy(c)))
+        return outs
+
+    return compute
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1201_2025_b200 import DetectRequest, WindowConfig
+        from paper_1201_2025_b200.sharded import run_sharded
+        cube = oracle.port.random_cube(LINES, SAMPLES, BANDS, 4242)
+        reqs = [DetectRequest("lrx", WindowConfig.single(7)),
+                DetectRequest("dwrx", WindowConfig.dual(3, 9)),
+                DetectRequest("dwest", WindowConfig.dual(3, 9), eigcount=True)]
+        plan, maps, counts = run_sharded(
+            lambda b0, b1: torch.from_numpy(cube[b0:b1].copy()), LINES, SAMPLES, reqs, dist,
+            compute=_oracle_compute(cube))
+        if rank == 0:
+            q.put(("maps", [m.numpy() for m in maps], counts[2].numpy(), plan.per))
+        q.put(("plan", rank, plan.r0, plan.r1, plan.b0, plan.nb))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gather_equals_single_process(orc, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    got = {}
+    plans = []
+    while not q.empty():
+        item = q.get()
+        if item[0] == "maps":
+            got = item
+        else:
+            plans.append(item[1:])
+    _, maps, counts, per = got
+    cube = orc.port.random_cube(LINES, SAMPLES, BANDS, 4242)
+    red = orc.port.reduce_cube(cube, 2, 4)
+    want = [orc.port.local_rx(red, 7), orc.port.dwrx(red, 3, 9)]
+    ds, dc = orc.port.dwest(red, 3, 9)
+    want.append(ds)
+    for m, w in zip(maps, want):
+        assert np.all(np.isfinite(m)), "a rank read outside its halo"
+        assert np.array_equal(m, w)
+    assert np.array_equal(counts, dc)
+    # strips tile the image; buffers are strip + halo within the image
+    plans.sort()
+    assert plans[0][1] == 0 and plans[-1][2] == LINES
+    for (_, r0, r1, b0, nb) in plans:
+        if r1 > r0:
+            assert b0 <= max(0, r0 - 4) and b0 + nb >= min(LINES, r1 + 4)
