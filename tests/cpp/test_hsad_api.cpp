@@ -1,0 +1,158 @@
+// C++ drop-in test: the reference's own unit cases (proj/tests/test_wavelet.cpp,
+// test_detect.cpp) written against include/hsad/hsad_b200.hpp, i.e. the same
+// hsad:: calls a reference user makes, running on the sm_100a kernels.
+// Built and run by tests/test_cpp_api.py (-m gpu). Exit code = failures.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "hsad/hsad_b200.hpp"
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                              \
+    do {                                                                         \
+        if (cond) ++g_pass;                                                      \
+        else {                                                                   \
+            ++g_fail;                                                            \
+            std::fprintf(stderr, "%s:%d: CHECK failed: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                        \
+    } while (0)
+#define CHECK_THROWS_CODE(expr, ec)                                              \
+    do {                                                                         \
+        bool thrown = false;                                                     \
+        try {                                                                    \
+            (void)(expr);                                                        \
+        } catch (const hsad::Error& e) {                                         \
+            thrown = e.code() == (ec);                                           \
+        }                                                                        \
+        CHECK(thrown);                                                           \
+    } while (0)
+
+namespace {
+// xoshiro256++ / splitmix64 (proj/core/include/hsad/rng.hpp:13-64) for random_cube
+struct Rng {
+    uint64_t s[4];
+    explicit Rng(uint64_t seed) {
+        uint64_t x = seed;
+        for (auto& w : s) {
+            x += 0x9e3779b97f4a7c15ULL;
+            uint64_t z = x;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            w = z ^ (z >> 31);
+        }
+    }
+    static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+    uint64_t next() {
+        const uint64_t r = rotl(s[0] + s[3], 23) + s[0], t = s[1] << 17;
+        s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t; s[3] = rotl(s[3], 45);
+        return r;
+    }
+    double u01() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+hsad::HyperCube random_cube(int l, int s, int b, uint64_t seed) {
+    Rng rng(seed);
+    hsad::HyperCube c(l, s, b);
+    for (auto& v : c.values) v = rng.u01();
+    return c;
+}
+void set_pixel(hsad::HyperCube& c, int r, int col, double a, double b) {
+    c.at(r, col, 0) = a;
+    c.at(r, col, 1) = b;
+}
+hsad::HyperCube hand_cube(double cx, double cy) {
+    hsad::HyperCube cube(3, 3, 2);
+    set_pixel(cube, 0, 0, 2, 0);
+    set_pixel(cube, 0, 1, 0, 2);
+    set_pixel(cube, 0, 2, -2, 0);
+    set_pixel(cube, 1, 0, 0, -2);
+    set_pixel(cube, 1, 1, cx, cy);
+    return cube;
+}
+}  // namespace
+
+int main() {
+    using namespace hsad;
+    // test_wavelet.cpp:54-65, 67-71
+    auto f = daubechies_filters(2);
+    CHECK(std::abs(f.low[0] - 0.4829629131) < 1e-10 && std::abs(f.low[3] + 0.1294095226) < 1e-10);
+    CHECK_THROWS_CODE(daubechies_filters(0), errc::unsupported_order);
+    CHECK_THROWS_CODE(daubechies_filters(11), errc::unsupported_order);
+    // test_wavelet.cpp:196-210: shape and constant gain
+    auto red = reduce_cube(random_cube(6, 10, 64, 21), f, 4);
+    CHECK(red.lines() == 6 && red.samples() == 10 && red.bands() == 4);
+    HyperCube flat(3, 4, 64);
+    for (auto& v : flat.values) v = 0.5;
+    bool gain_ok = true;
+    for (double v : reduce_cube(flat, f, 4).values) gain_ok = gain_ok && std::abs(v - 2.0) < 1e-10;
+    CHECK(gain_ok);
+    HyperCube c189(2, 2, 189);
+    for (auto& v : c189.values) v = 2.0;
+    bool gain8 = true;
+    for (double v : reduce_cube(c189, f, 4).values) gain8 = gain8 && std::abs(v - 16.0) < 1e-9;
+    CHECK(gain8);
+    CHECK_THROWS_CODE(reduce_cube(flat, f, 3), errc::invalid_value);
+    CHECK_THROWS_CODE(reduce_cube(flat, f, 128), errc::target_too_large);
+
+    // test_detect.cpp:23-43
+    CHECK(mirror_index(-1, 5) == 1 && mirror_index(9, 5) == 1 && mirror_index(-7, 3) == 1 &&
+          mirror_index(3, 1) == 0);
+    CHECK_THROWS_CODE(WindowConfig::single(2), errc::invalid_value);
+    CHECK_THROWS_CODE(WindowConfig::dual(5, 6), errc::invalid_value);
+    CHECK(WindowConfig::single(15).describe() == "15" && WindowConfig::dual(5, 13).describe() == "5/13");
+
+    // test_detect.cpp:76-91, 112-121: hand cases
+    auto m = local_rx(hand_cube(3, 4), WindowConfig::single(3), 1e-9);
+    CHECK(std::abs(m.at(1, 1) - 25.0) < 25e-6);
+    CHECK(m.algorithm == "lrx" && m.window == "3");
+    CHECK(std::abs(dwrx(hand_cube(1, 2), WindowConfig::dual(1, 3), 1e-9).at(1, 1) - 5.0) < 5e-6);
+    // test_detect.cpp:93-98, 123-135: constant fields
+    HyperCube k(9, 9, 3);
+    for (auto& v : k.values) v = 0.75;
+    bool zero = true;
+    for (double s : local_rx(k, WindowConfig::single(3), 1e-6).scores) zero = zero && s == 0.0;
+    for (double s : dwrx(k, WindowConfig::dual(3, 7), 1e-6).scores) zero = zero && s == 0.0;
+    for (double s : dwest(k, WindowConfig::dual(3, 7), DwestConfig{}).scores) zero = zero && s == 0.0;
+    CHECK(zero);
+    // test_detect.cpp:172-182: finite and non-negative
+    auto cube = random_cube(9, 9, 3, 77);
+    bool fin = true;
+    for (const auto& mm : {local_rx(cube, WindowConfig::single(5), 1e-6),
+                           dwrx(cube, WindowConfig::dual(3, 7), 1e-6),
+                           dwest(cube, WindowConfig::dual(3, 7), DwestConfig{})})
+        for (double s : mm.scores) fin = fin && std::isfinite(s) && s >= 0.0;
+    CHECK(fin);
+    // test_detect.cpp:184-203: translation invariance
+    auto c8 = random_cube(8, 8, 3, 31);
+    auto sh = c8;
+    const double off[3] = {5.0, -2.0, 11.0};
+    for (size_t i = 0; i < sh.values.size(); ++i) sh.values[i] += off[i % 3];
+    auto rel = [](const ScoreMap& a, const ScoreMap& b) {
+        double w = 0;
+        for (size_t i = 0; i < a.scores.size(); ++i)
+            w = std::max(w, std::abs(a.scores[i] - b.scores[i]) /
+                                std::max({1.0, std::abs(a.scores[i]), std::abs(b.scores[i])}));
+        return w;
+    };
+    CHECK(rel(local_rx(c8, WindowConfig::single(5), 1e-6), local_rx(sh, WindowConfig::single(5), 1e-6)) < 1e-8);
+    CHECK(rel(dwest(c8, WindowConfig::dual(3, 7), DwestConfig{}), dwest(sh, WindowConfig::dual(3, 7), DwestConfig{})) < 1e-8);
+    // test_detect.cpp:235-249: dispatch checks the window mode
+    auto c61 = random_cube(8, 8, 3, 61);
+    CHECK(detect(c61, Algorithm::LRX, WindowConfig::single(5)).algorithm == "lrx");
+    CHECK_THROWS_CODE(detect(c61, Algorithm::DWEST, WindowConfig::single(15)), errc::config_mismatch);
+    CHECK_THROWS_CODE(detect(c61, Algorithm::LRX, WindowConfig::dual(3, 7)), errc::config_mismatch);
+    // per-pixel error path: "... at pixel (r, c)" (detect.cpp:127-130)
+    HyperCube z(5, 5, 2);
+    set_pixel(z, 2, 2, 1.0, 1.0);
+    bool msg_ok = false;
+    try {
+        local_rx(z, WindowConfig::single(3), 1e-6);
+    } catch (const Error& e) {
+        msg_ok = e.code() == errc::singular_after_ridge &&
+                 std::string(e.what()).find("at pixel (2, 2)") != std::string::npos;
+    }
+    CHECK(msg_ok);
+    std::printf("cpp drop-in: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail;
+}
