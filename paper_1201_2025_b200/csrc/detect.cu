@@ -33,6 +33,9 @@
 #include "hsad_internal.h"
 
 namespace hsad_b200 {
+
+hsad_status fullband_launch(FbParams& P, cudaStream_t s);
+
 namespace {
 
 constexpr int kCodeOverflow = 0x80;  // flag: "inverse overflowed" variant of SingularAfterRidge
@@ -883,11 +886,17 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     if (st != HSAD_OK) return st;
     if (elem_bytes != 4 && elem_bytes != 8)
         return set_error(HSAD_E_INVALID_VALUE, "elem_bytes must be 4 or 8");
-    if (bands < 1 || bands > kMaxDetectBands)
-        return set_error(HSAD_E_UNSUPPORTED, "hsad_detect supports 1.." +
-                                                 std::to_string(kMaxDetectBands) +
-                                                 " bands (reduce the cube first), got " +
-                                                 std::to_string(bands));
+    // bands > 8: the full-band path (K5/K6, fullband.cu) for LRX / DWRX
+    const bool fullband = bands > kMaxDetectBands;
+    if (bands < 1) return set_error(HSAD_E_INVALID_VALUE, "cube has no bands");
+    if (fullband)
+        for (int q = 0; q < n_requests; ++q)
+            if (requests[q].algorithm == HSAD_DWEST)
+                return set_error(HSAD_E_UNSUPPORTED,
+                                 "full-band DWEST (" + std::to_string(bands) +
+                                     " bands) is not in this build; reduce the cube first "
+                                     "(hsad_reduce) or use <= " +
+                                     std::to_string(kMaxDetectBands) + " bands");
     if (lines < 0 || samples < 0 || row_begin < 0 || row_end > lines || row_begin > row_end)
         return set_error(HSAD_E_INVALID_VALUE, "row range outside the image");
     if (row_begin == row_end || samples == 0) return HSAD_OK;
@@ -939,11 +948,12 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     // <= 56 KB keeps 4 CTAs per SM (228 KB shared memory); K shrinks to fit
     const int64_t smem_cap = getenv("HSAD_SMEM_CAP_KB") ? atoi(getenv("HSAD_SMEM_CAP_KB")) * 1024 : 56 * 1024;
     while (kc > 1 && smem_for(kc) > smem_cap) kc /= 2;
-    if (smem_for(kc) > 227 * 1024)
+    if (!fullband && smem_for(kc) > 227 * 1024)
         return set_error(HSAD_E_UNSUPPORTED,
                          "window statistics for " + std::to_string(P.nbox) + " window sizes up to " +
                              std::to_string(2 * P.rmax + 1) + " at " + std::to_string(bands) +
                              " bands exceed shared memory; split the requests");
+    if (fullband) kc = 1;
     plan.kcols = kc;
     P.tw = 128 * kc;
     P.diag_lin = -1;
@@ -962,8 +972,43 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     }
     P.status = status;
-    cudaError_t e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
-    if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
+    // full-band launcher: one fullband_kernel launch per request over rows [rb, re)
+    auto launch_fb = [&](int64_t rb, int64_t re, int64_t diag_lin, double* diag_out,
+                         char* scratch) -> hsad_status {
+        for (int q = 0; q < n_requests; ++q) {
+            const hsad_detect_request& R = requests[q];
+            FbParams F{};
+            F.cube = d_cube;
+            F.elem_bytes = elem_bytes;
+            F.lines = lines;
+            F.samples = samples;
+            F.bands = bands;
+            F.buf_row0 = buf_row0;
+            F.row_begin = rb;
+            F.row_end = re;
+            F.algo = R.algorithm;
+            F.outer = R.algorithm == HSAD_LRX ? R.window.single_size : R.window.outer_size;
+            F.inner = R.algorithm == HSAD_LRX ? (R.guard <= 0 ? 1 : R.guard) : R.window.inner_size;
+            F.ridge = R.ridge;
+            F.scores = scratch ? static_cast<void*>(scratch + static_cast<size_t>(samples) * 9 * q)
+                               : R.d_scores;
+            F.score_bytes = R.score_bytes;
+            F.status = status;
+            F.diag_lin = diag_lin;
+            F.diag_out = diag_out;
+            hsad_status fst = fullband_launch(F, s);
+            if (fst != HSAD_OK) return fst;
+        }
+        return HSAD_OK;
+    };
+    cudaError_t e = cudaSuccess;
+    if (fullband) {
+        hsad_status fst = launch_fb(row_begin, row_end, -1, nullptr, nullptr);
+        if (fst != HSAD_OK) return fst;
+    } else {
+        e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
+        if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
+    }
     if (!sync) return HSAD_OK;
 
     unsigned long long packed = 0;
@@ -998,7 +1043,11 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                     D.req[q].eigcount = reinterpret_cast<int8_t*>(
                         scratch + static_cast<size_t>(samples) * (9 * q + 8));
             }
-            e = launch_detect(bands, D, dim3(plan.grid.x, 1), plan.nt, plan.kcols, s);
+            if (fullband) {
+                if (launch_fb(row, row + 1, lin, d_diag, scratch) != HSAD_OK) e = cudaErrorUnknown;
+            } else {
+                e = launch_detect(bands, D, dim3(plan.grid.x, 1), plan.nt, plan.kcols, s);
+            }
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(&delta, d_diag, sizeof(double), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);

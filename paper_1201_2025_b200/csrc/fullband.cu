@@ -1,0 +1,289 @@
+// K5+K6: full-band detectors (bands > 8, e.g. BASELINE C3: LRX on the raw 189-band cube).
+// hsad::local_rx / hsad::dwrx at any band count (proj/core/src/detect.cpp:159-228 with
+// stats.cpp:7-62): explicit window gather, two-pass centred covariance (divisor N),
+// ridge delta = r tr(C)/L, Cholesky, quadratic form.
+//
+// One CTA (256 threads) per output pixel:
+//   1. pass 1: window means (threads over bands, samples in the reference's scan order);
+//   2. pass 2: centred samples stream through shared memory in chunks; every thread
+//      owns up to 5 register-tiled 4x4 blocks of the lower triangle of the Gram
+//      matrix and accumulates them in fp64 (N L^2 MACs: the dense contraction);
+//   3. the bordered matrix [C + delta I, d; d^T, 0] is written packed (lower, row-major)
+//      to shared memory and factorised in place (right-looking Cholesky, one column
+//      per step). The last Schur pivot is 0 - d^T (C + delta I)^-1 d, i.e. minus the
+//      score, so no triangular solve is needed. D_j = pivots (singular rule as K3).
+// Supports bands <= 224 (packed bordered matrix <= 209 KB of shared memory).
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "hsad_internal.h"
+
+namespace hsad_b200 {
+
+constexpr int kFbThreads = 256;
+constexpr int kFbMaxBands = 224;
+constexpr int kFbMaxTiles = 5;  // 4x4 Gram tiles per thread (lower triangle of 228 x 228)
+
+namespace {
+
+__device__ __forceinline__ int mirror_fb(int i, int n) {
+    if (static_cast<unsigned>(i) < static_cast<unsigned>(n)) return i;
+    if (n == 1) return 0;
+    const int period = 2 * (n - 1);
+    i = abs(i) % period;
+    return i < n ? i : period - i;
+}
+
+__device__ __forceinline__ double ld(const FbParams& P, int64_t idx) {
+    return P.elem_bytes == 8 ? __ldg(static_cast<const double*>(P.cube) + idx)
+                             : static_cast<double>(__ldg(static_cast<const float*>(P.cube) + idx));
+}
+
+// element index of window sample s (reference scan order: dr outer, dc inner,
+// skipping the excluded centred box of edge `excl`, 0 = none) of pixel (r, c)
+__device__ __forceinline__ int64_t sample_base(const FbParams& P, int r, int c, int s, int size,
+                                               int excl) {
+    const int h = size / 2, eh = excl / 2;
+    // the excluded box occupies rows |dr| <= eh, columns |dc| <= eh
+    int dr, dc;
+    if (excl <= 0) {
+        dr = s / size - h;
+        dc = s % size - h;
+    } else {
+        const int top = (h - eh) * size;  // samples in the rows above the excluded band
+        if (s < top) {
+            dr = s / size - h;
+            dc = s % size - h;
+        } else {
+            const int mid_rows = 2 * eh + 1, per_mid = size - excl;
+            const int sm = s - top;
+            if (sm < mid_rows * per_mid) {
+                dr = sm / per_mid - eh;
+                const int k = sm % per_mid;
+                dc = k < h - eh ? k - h : k - (h - eh) + eh + 1;
+            } else {
+                const int sb = sm - mid_rows * per_mid;
+                dr = eh + 1 + sb / size;
+                dc = sb % size - h;
+            }
+        }
+    }
+    const int rr = mirror_fb(r + dr, static_cast<int>(P.lines)) - static_cast<int>(P.buf_row0);
+    const int cc = mirror_fb(c + dc, static_cast<int>(P.samples));
+    return (static_cast<int64_t>(rr) * P.samples + cc) * P.bands;
+}
+
+__device__ __forceinline__ int packed(int i, int k) { return i * (i + 1) / 2 + k; }  // k <= i
+
+__global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams P) {
+    extern __shared__ double sm[];
+    const int L = P.bands, MP = P.mp, CH = P.chunk;
+    double* A = sm;                                   // packed (MP x MP lower)
+    double* xs = A + packed(MP - 1, MP - 1) + 1;      // [CH][MP] centred samples
+    double* mu = xs + static_cast<int64_t>(CH) * MP;  // [2][MP] means (window / inner box)
+    double* col = mu + 2 * MP;                        // [MP] current Cholesky column
+    __shared__ double s_piv, s_dmax, s_dmin;
+    __shared__ int s_bad;
+
+    const int t = threadIdx.x;
+    const int c = blockIdx.x;
+    const int64_t r = P.row_begin + blockIdx.y;
+    if (r >= P.row_end) return;
+    const int ri = static_cast<int>(r);
+    // sample sets: LRX background = window minus the guard box (centre when guard 1);
+    // DWRX covariance = annulus (outer minus inner box), d = mean(inner) - mean(annulus)
+    const int size = P.outer;
+    const int excl = P.inner;
+    const int N = size * size - excl * excl;
+
+    // pass 1: means
+    for (int b = t; b < MP; b += kFbThreads) {
+        double s = 0.0, si = 0.0;
+        if (b < L) {
+            for (int k = 0; k < N; ++k) s += ld(P, sample_base(P, ri, c, k, size, excl) + b);
+            if (P.algo == HSAD_DWRX)
+                for (int k = 0; k < excl * excl; ++k)
+                    si += ld(P, sample_base(P, ri, c, k, excl, 0) + b);
+        }
+        mu[b] = b < L ? s / N : 0.0;
+        mu[MP + b] = (b < L && P.algo == HSAD_DWRX) ? si / (excl * excl) : 0.0;
+    }
+    __syncthreads();
+
+    // pass 2: centred Gram, 4x4 tiles of the lower triangle, in groups of
+    // kFbThreads * kFbMaxTiles tiles (one group for L <= 196, two for L = 224)
+    const int T = MP / 4;
+    const int ntiles = T * (T + 1) / 2;
+    const double invN = 1.0 / N;
+    for (int g0 = 0; g0 < ntiles; g0 += kFbThreads * kFbMaxTiles) {
+        int ti[kFbMaxTiles], tj[kFbMaxTiles];
+        double acc[kFbMaxTiles][4][4];
+#pragma unroll
+        for (int u = 0; u < kFbMaxTiles; ++u) {
+            const int tile = g0 + t + u * kFbThreads;
+            int a = static_cast<int>((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+            while ((a + 1) * (a + 2) / 2 <= tile) ++a;
+            while (a * (a + 1) / 2 > tile) --a;
+            ti[u] = tile < ntiles ? a : -1;
+            tj[u] = tile < ntiles ? tile - a * (a + 1) / 2 : -1;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[u][i][j] = 0.0;
+        }
+        for (int k0 = 0; k0 < N; k0 += CH) {
+            const int nk = min(CH, N - k0);
+            __syncthreads();
+            for (int e = t; e < nk * MP; e += kFbThreads) {
+                const int k = e / MP, b = e % MP;
+                xs[e] = b < L ? ld(P, sample_base(P, ri, c, k0 + k, size, excl) + b) - mu[b] : 0.0;
+            }
+            __syncthreads();
+            for (int k = 0; k < nk; ++k) {
+                const double* x = xs + k * MP;
+#pragma unroll
+                for (int u = 0; u < kFbMaxTiles; ++u) {
+                    if (ti[u] < 0) continue;
+                    const double2 a01 = *reinterpret_cast<const double2*>(x + 4 * ti[u]);
+                    const double2 a23 = *reinterpret_cast<const double2*>(x + 4 * ti[u] + 2);
+                    const double2 b01 = *reinterpret_cast<const double2*>(x + 4 * tj[u]);
+                    const double2 b23 = *reinterpret_cast<const double2*>(x + 4 * tj[u] + 2);
+                    const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+                    const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[u][i][j] = fma(av[i], bv[j], acc[u][i][j]);
+                }
+            }
+        }
+        // covariance (divisor N) into packed lower storage; symmetric by construction
+#pragma unroll
+        for (int u = 0; u < kFbMaxTiles; ++u) {
+            if (ti[u] < 0) continue;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int gi = 4 * ti[u] + i, gj = 4 * tj[u] + j;
+                    if (gj <= gi) A[packed(gi, gj)] = acc[u][i][j] * invN;
+                }
+        }
+    }
+    __syncthreads();
+    // displacement d and ridge; border row L holds d, (L, L) = 0; rows > L are inert
+    if (t == 0) {
+        double tr = 0.0;
+        for (int b = 0; b < L; ++b) tr += A[packed(b, b)];
+        s_piv = P.ridge * tr / L;  // delta
+        s_bad = 0;
+        s_dmax = 0.0;
+        s_dmin = DBL_MAX;
+    }
+    __syncthreads();
+    const double delta = s_piv;
+    double dmaxabs = 0.0;
+    for (int b = t; b < MP; b += kFbThreads) {
+        if (b < L) {
+            A[packed(b, b)] += delta;
+            double d;
+            if (P.algo == HSAD_LRX) {
+                const int rr = mirror_fb(ri, static_cast<int>(P.lines)) - static_cast<int>(P.buf_row0);
+                d = ld(P, (static_cast<int64_t>(rr) * P.samples + c) * L + b) - mu[b];
+            } else {
+                d = mu[MP + b] - mu[b];
+            }
+            A[packed(L, b)] = d;
+            dmaxabs = fmax(dmaxabs, fabs(d));
+        } else if (b == L) {
+            A[packed(L, L)] = 0.0;  // border corner; rows > L (padding) are never read
+        }
+    }
+    // any non-zero displacement? (detect.cpp:175-177 / 212: zero d skips the inverse)
+    const int any_d = __syncthreads_or(dmaxabs > 0.0);
+    const int64_t o = (r - P.row_begin) * P.samples + c;
+    const int64_t lin = r * P.samples + c;
+    if (lin == P.diag_lin && t == 0) *P.diag_out = delta;
+    double score = 0.0;
+    if (any_d) {
+        // right-looking Cholesky of the bordered matrix, rows 0..L
+        for (int j = 0; j <= L; ++j) {
+            if (t == 0) {
+                const double p = A[packed(j, j)];
+                if (j < L) {
+                    if (!(p > 0.0)) s_bad = 1;
+                    s_dmax = fmax(s_dmax, fabs(p));
+                    s_dmin = fmin(s_dmin, p);
+                }
+                s_piv = p;
+            }
+            __syncthreads();
+            if (s_bad || j == L) break;
+            const double rinv = rsqrt(s_piv);
+            for (int i = j + 1 + t; i <= L; i += kFbThreads) {
+                const double v = A[packed(i, j)] * rinv;
+                A[packed(i, j)] = v;
+                col[i] = v;
+            }
+            __syncthreads();
+            // trailing update: rows i > j, columns j < k <= i; warps over rows, lanes over k
+            const int warp = t >> 5, lane = t & 31;
+            for (int i = j + 1 + warp; i <= L; i += kFbThreads / 32) {
+                const double lij = col[i];
+                double* row = A + packed(i, 0);
+                for (int k = j + 1 + lane; k <= i; k += 32) row[k] = fma(-lij, col[k], row[k]);
+            }
+            __syncthreads();
+        }
+        if (t == 0) {
+            const bool singular = s_bad || !(s_dmax > 0.0) || s_dmin <= s_dmax * 1e-14;
+            if (singular) {
+                const unsigned long long packedc =
+                    (static_cast<unsigned long long>(lin) << 8) | HSAD_E_SINGULAR_AFTER_RIDGE;
+                atomicMin(P.status, packedc);
+            } else {
+                score = -s_piv;  // Schur complement: 0 - d^T (C + delta I)^-1 d
+                if (!isfinite(score)) {
+                    atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
+                                            (HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
+                    score = 0.0;
+                }
+            }
+        }
+    }
+    if (t == 0) {
+        score = P.algo == HSAD_LRX ? fmax(score, 0.0) : fabs(score);
+        if (P.score_bytes == 8) static_cast<double*>(P.scores)[o] = score;
+        else static_cast<float*>(P.scores)[o] = static_cast<float>(score);
+    }
+}
+
+}  // namespace
+
+// Shared memory and launch shape for one full-band request.
+hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
+    if (P.bands > kFbMaxBands)
+        return set_error(HSAD_E_UNSUPPORTED, "full-band detection supports at most " +
+                                                 std::to_string(kFbMaxBands) + " bands");
+    P.mp = ((P.bands + 1) + 3) / 4 * 4;
+    const int64_t tri = static_cast<int64_t>(P.mp) * (P.mp + 1) / 2;
+    int chunk = 32;
+    auto bytes = [&](int ch) { return (tri + static_cast<int64_t>(ch) * P.mp + 3 * P.mp) * 8; };
+    while (chunk > 4 && bytes(chunk) > 220 * 1024) chunk /= 2;
+    if (bytes(chunk) > 227 * 1024)
+        return set_error(HSAD_E_UNSUPPORTED, "full-band working set exceeds shared memory");
+    P.chunk = chunk;
+    const size_t smem = static_cast<size_t>(bytes(chunk));
+    HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    const int64_t rows = P.row_end - P.row_begin;
+    if (rows > 65535) return set_error(HSAD_E_UNSUPPORTED, "strip too tall for one launch");
+    dim3 grid(static_cast<unsigned>(P.samples), static_cast<unsigned>(rows));
+    fullband_kernel<<<grid, kFbThreads, smem, s>>>(P);
+    HSAD_CUDA_TRY(cudaGetLastError());
+    return HSAD_OK;
+}
+
+}  // namespace hsad_b200

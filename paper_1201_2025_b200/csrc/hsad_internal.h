@@ -40,6 +40,27 @@ hsad_status wavelet_plan(int32_t bands, int32_t order, int32_t target, std::vect
 
 hsad_status window_validate(const hsad_window& w);
 
+// Full-band (bands > 8) LRX / DWRX request, fullband.cu.
+struct FbParams {
+    const void* cube;
+    int elem_bytes;
+    int64_t lines, samples;
+    int bands;
+    int64_t buf_row0;
+    int64_t row_begin, row_end;
+    int algo;           // HSAD_LRX or HSAD_DWRX
+    int outer;          // LRX window / DWRX outer
+    int inner;          // LRX guard (1 = centre only) / DWRX inner
+    double ridge;
+    void* scores;
+    int score_bytes;
+    unsigned long long* status;
+    int64_t diag_lin;
+    double* diag_out;
+    int chunk;          // samples per shared-memory chunk (set by fullband_launch)
+    int mp;             // bordered dimension L+1 rounded up to a multiple of 4
+};
+
 // Kernel-side limits.
 constexpr int kMaxDetectBands = 8;
 constexpr int kMaxBoxes = 4;

@@ -339,3 +339,67 @@ def test_golden_vectors_from_reference_code():
     assert max_rel_diff(host(hs.local_rx(c, W1(7)).scores), g["lrx7_99"]) < 1e-10
     assert max_rel_diff(host(hs.dwrx(c, W2(5, 9)).scores), g["dwrx59_99"]) < 1e-10
     assert max_rel_diff(host(hs.dwest(c, W2(5, 9), 0.3).scores), g["dwest59_99"]) < 1e-10
+
+
+# ------------------------------------------------------------------ full-band path (K5/K6)
+def _fb_kappa(cube, rows, size, excl, ridge):
+    """Condition numbers of the ridged background covariances of the given rows."""
+    L, S, B = cube.shape
+    h, eh = size // 2, excl // 2
+    offs = [(dr, dc) for dr in range(-h, h + 1) for dc in range(-h, h + 1)
+            if not (excl > 0 and abs(dr) <= eh and abs(dc) <= eh)]
+    out = np.zeros((rows[1] - rows[0], S))
+    for i, r in enumerate(range(*rows)):
+        for c in range(S):
+            X = np.array([cube[_mirror(np.array(r + dr), L), _mirror(np.array(c + dc), S)]
+                          for dr, dc in offs])
+            C = np.cov(X.T, bias=True)
+            C += ridge * np.trace(C) / B * np.eye(B)
+            out[i, c] = np.linalg.cond(C)
+    return out
+
+
+@pytest.mark.parametrize("bands,window,inner,outer", [(12, 7, 3, 7), (30, 9, 3, 9), (61, 11, 5, 11)])
+def test_fullband_random_cubes(orc, bands, window, inner, outer):
+    cube = orc.port.random_cube(11, 13, bands, 500 + bands)
+    (l, _), (d, _) = run(cube, [hs.DetectRequest("lrx", W1(window)),
+                                hs.DetectRequest("dwrx", W2(inner, outer))])
+    assert_kappa_close(l, orc.port.local_rx(cube, window), _fb_kappa(cube, (0, 11), window, 1, 1e-6),
+                       f"fullband lrx L={bands}")
+    assert_kappa_close(d, orc.port.dwrx(cube, inner, outer),
+                       _fb_kappa(cube, (0, 11), outer, inner, 1e-6), f"fullband dwrx L={bands}")
+    # guard extension at full band
+    (g, _), = run(cube, [hs.DetectRequest("lrx", W1(window), guard=3)])
+    assert_kappa_close(g, orc.port.local_rx(cube, window, guard=3),
+                       _fb_kappa(cube, (0, 11), window, 3, 1e-6), f"fullband lrx guard L={bands}")
+
+
+def test_fullband_config_c3(orc):
+    """BASELINE C3: 100x100x189 without DWT, LRX 15 (reference) and 15/5 guard; rows 0..6
+    and 47..52 compared with the oracle (kappa-aware: cond ~1e6-1e7 at 189 bands)."""
+    cfg = CONFIGS["C3"]
+    cube, _ = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], cfg["rate"],
+                             device=DEV)
+    (l, _), (g, _) = [(host(s), c) for s, c in hs.detect_multi(
+        cube, [hs.DetectRequest("lrx", W1(15)), hs.DetectRequest("lrx", W1(15), guard=5)])]
+    ch = host(cube)
+    for rows in ((0, 6), (47, 52)):
+        want = orc.port.local_rx(ch, 15, 1e-6, workers=8, rows=rows)
+        kap = _fb_kappa(ch.astype(np.float64), rows, 15, 1, 1e-6)
+        assert_kappa_close(l[rows[0]:rows[1]], want, kap, f"C3 lrx rows {rows}")
+        wg = orc.port.local_rx(ch, 15, 1e-6, guard=5, workers=8, rows=rows)
+        kg = _fb_kappa(ch.astype(np.float64), rows, 15, 5, 1e-6)
+        assert_kappa_close(g[rows[0]:rows[1]], wg, kg, f"C3 lrx guard rows {rows}")
+
+
+def test_fullband_dwest_unsupported_and_errors(orc):
+    cube = gpu(orc.port.random_cube(6, 6, 20, 3))
+    with pytest.raises(hs.HsadError) as e:
+        hs.dwest(cube, W2(3, 5))
+    assert e.value.name == "Unsupported"
+    flat = np.zeros((5, 5, 12)); flat[2, 2] = 1.0
+    with pytest.raises(OracleError) as want:
+        orc.port.local_rx(flat, 3, 1e-6)
+    with pytest.raises(hs.HsadError) as got:
+        hs.local_rx(gpu(flat), W1(3), 1e-6)
+    assert str(got.value) == str(want.value)
