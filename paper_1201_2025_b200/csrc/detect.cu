@@ -66,6 +66,9 @@ struct DetectParams {
     int radius[kMaxBoxes];
     int nreq;
     ReqDev req[kMaxRequests];
+    int std_layout;  // box 0 = LRX/outer window for every request, box 1 = inner box
+    int has_dual;
+    double n_in, n_ann;  // standard-layout dual counts
     unsigned long long* status;
     int64_t diag_lin;   // >= 0: pixel whose ridge delta is written to diag_out
     double* diag_out;
@@ -86,12 +89,14 @@ __device__ __forceinline__ void report(const DetectParams& P, int64_t row, int64
 }
 
 // Reflection on int32 coordinates with the in-range case first (detect.cpp:71-76).
-__device__ __forceinline__ int mirror32(int i, int n) {
-    if (static_cast<unsigned>(i) < static_cast<unsigned>(n)) return i;
+__device__ __noinline__ int mirror32_slow(int i, int n) {
     if (n == 1) return 0;
     const int period = 2 * (n - 1);
     i = abs(i) % period;
     return i < n ? i : period - i;
+}
+__device__ __forceinline__ int mirror32(int i, int n) {
+    return static_cast<unsigned>(i) < static_cast<unsigned>(n) ? i : mirror32_slow(i, n);
 }
 
 // y = spectrum at (global row vrow, this thread's data column) as fp64
@@ -254,11 +259,17 @@ __device__ __forceinline__ void rotate_tc(T (&a)[L][L], T (&v)[L][L], int p, int
 
 // fp32 Jacobi angle (MUFU only): t = sgn(th)/(|th| + sqrt(th^2 + 1)),
 // th = (a_qq - a_pp)/(2 a_pq); a_pq == 0 gives the identity rotation.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float jacobi_t32(float app, float aqq, float apq) {
-    const float th = 0.5f * __fdividef(aqq - app, apq);
+    const float th = 0.5f * (aqq - app) * rcp_approx(apq);
     const float ath = fabsf(th);
     const float r = fmaf(th, th, 1.0f);
-    float t = ath > 1e15f ? __fdividef(0.5f, ath) : __fdividef(1.0f, ath + r * rsqrtf(r));
+    // |th| > 1e15: th^2 overflows; t -> 1/(2|th|). rcp.approx(inf) = 0 covers a_pq == 0.
+    float t = ath > 1e15f ? 0.5f * rcp_approx(ath) : rcp_approx(ath + r * rsqrtf(r));
     t = th < 0.0f ? -t : t;
     return apq == 0.0f ? 0.0f : t;
 }
@@ -431,143 +442,193 @@ __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s
     else static_cast<float*>(R.scores)[o] = static_cast<float>(s);
 }
 
-// Per-pixel solves of every request from the box sums S (detect.cpp:168-271).
+// ---- per-detector solves on window statistics ---------------------------------
+
+// LRX (detect.cpp:168-188) on background sums bg, count n: score = max(d^T (C+dI)^-1 d, 0)
+template <int L>
+__device__ __forceinline__ void lrx_solve(const DetectParams& P, const ReqDev& R,
+                                          const double (&bg)[Dim<L>::NC], double n_bg,
+                                          const double (&yc)[L], int64_t r, int64_t col, int64_t o,
+                                          int64_t lin) {
+    double mu[L], cm[L][L], dv[L];
+    mean_cov<L>(bg, n_bg, mu, cm);
+    double dmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        dv[i] = yc[i] - mu[i];
+        dmax = fmax(dmax, fabs(dv[i]));
+    }
+    double score = 0.0;
+    if (dmax > 0.0) {
+        double delta = 0.0;
+        const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
+        if (lin == P.diag_lin) *P.diag_out = delta;
+        if (code) {
+            report(P, r, col, code);
+            score = 0.0;
+        }
+    }
+    store_score(R, o, fmax(score, 0.0));
+}
+
+// inner-box / annulus statistics shared by DWRX and DWEST (detect.cpp:204-213, 244-253)
+template <int L>
+struct DualStats {
+    double c_in[L][L], c_out[L][L], md[L], mmax;
+};
+template <int L>
+__device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
+                                           const double (&s_box)[Dim<L>::NC], double n_in,
+                                           double n_ann, DualStats<L>& D) {
+    constexpr int NC = Dim<L>::NC;
+    double sann[NC], mu_in[L], mu_out[L];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) sann[c] = s_box[c] - s_in[c];
+    mean_cov<L>(s_in, n_in, mu_in, D.c_in);
+    mean_cov<L>(sann, n_ann, mu_out, D.c_out);
+    D.mmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        D.md[i] = mu_in[i] - mu_out[i];
+        D.mmax = fmax(D.mmax, fabs(D.md[i]));
+    }
+}
+
+// DWRX (detect.cpp:204-223): |m^T (C_ann + dI)^-1 m|
+template <int L>
+__device__ __forceinline__ void dwrx_solve(const DetectParams& P, const ReqDev& R,
+                                           const DualStats<L>& D, int64_t r, int64_t col, int64_t o,
+                                           int64_t lin) {
+    double score = 0.0;
+    if (D.mmax > 0.0) {
+        double a[L][L];
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+#pragma unroll
+            for (int j = 0; j < L; ++j) a[i][j] = D.c_out[i][j];
+        double delta = 0.0;
+        const int code = chol_quad<L>(a, D.md, R.ridge, score, delta);
+        if (lin == P.diag_lin) *P.diag_out = delta;
+        if (code) {
+            report(P, r, col, code);
+            score = 0.0;
+        }
+    }
+    store_score(R, o, fabs(score));
+}
+
+// DWEST (detect.cpp:242-271)
+template <int L>
+__device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>& D, int64_t o) {
+    double cd[L][L], vec[L][L], w[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) cd[i][j] = D.c_in[i][j] - D.c_out[i][j];
+    dwest_eigen<L>(cd, vec, w);
+    // With eigenvalues sorted descending the reference loop sums v_i . m_diff while
+    // lambda_i > 0 && lambda_i >= f lambda0 and stops at the first failure
+    // (detect.cpp:255-262). The condition is monotone in lambda_i, so the summed set
+    // is exactly {i : lambda_i > 0, lambda_i >= f lambda0}: no sort needed. Sign rule
+    // (stats.cpp:83-85): v_i is flipped so its first largest-|.| component is positive.
+    double lmax = w[0];
+#pragma unroll
+    for (int i = 1; i < L; ++i) lmax = fmax(lmax, w[i]);
+    double score = 0.0;
+    int count = 0;
+    if (lmax > 0.0) {
+        const double cut = R.frac * lmax;
+        double proj = 0.0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            double best = fabs(vec[0][i]), lead = vec[0][i], dot = vec[0][i] * D.md[0];
+#pragma unroll
+            for (int k = 1; k < L; ++k) {
+                const double av = fabs(vec[k][i]);
+                lead = av > best ? vec[k][i] : lead;
+                best = fmax(best, av);
+                dot = fma(vec[k][i], D.md[k], dot);
+            }
+            const bool take = w[i] > 0.0 && !(w[i] < cut);
+            proj += take ? (lead < 0.0 ? -dot : dot) : 0.0;
+            count += take ? 1 : 0;
+        }
+        score = fabs(proj);
+    }
+    store_score(R, o, score);
+    if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
+}
+
 template <int L, int NBOX>
-__device__ __forceinline__ void solve_pixel(const DetectParams& P, const double (&S)[NBOX][Dim<L>::NC],
+__device__ __forceinline__ void select_box(const double (&S)[NBOX][Dim<L>::NC], int k,
+                                           double (&out)[Dim<L>::NC]) {
+#pragma unroll
+    for (int c = 0; c < Dim<L>::NC; ++c) out[c] = S[0][c];
+#pragma unroll
+    for (int kk = 1; kk < NBOX; ++kk)
+        if (k == kk) {
+#pragma unroll
+            for (int c = 0; c < Dim<L>::NC; ++c) out[c] = S[kk][c];
+        }
+}
+
+// Per-pixel solves of every request from the box sums S (detect.cpp:168-271).
+// Requests come from shared memory (s_req). In the standard layout — box 0 the
+// shared outer/LRX window, box 1 the inner box, LRX excluding only the centre —
+// box indices are compile-time and the inner/annulus statistics are computed
+// once for DWRX and DWEST; other layouts select boxes at run time.
+template <int L, int NBOX>
+__device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev* s_req,
+                                            const double (&S)[NBOX][Dim<L>::NC],
                                             const double (&yc)[L], int64_t r, int64_t col) {
     constexpr int NC = Dim<L>::NC;
     const int64_t o = (r - P.row_begin) * P.samples + col;
     const int64_t lin = r * P.samples + col;
+    if (P.std_layout) {
         for (int q = 0; q < P.nreq; ++q) {
-        // static indices only: a dynamic P.req[q] spills the param array to the stack
-        ReqDev R = P.req[0];
-#pragma unroll
-        for (int qq = 1; qq < kMaxRequests; ++qq)
-            if (q == qq) R = P.req[qq];
-        if (R.algo == HSAD_LRX) {
-            // detect.cpp:168-188: background = box - centre (or - guard box)
+            const ReqDev& R = s_req[q];
+            if (R.algo != HSAD_LRX) continue;
             double bg[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
-#pragma unroll
-            for (int k = 0; k < NBOX; ++k)
-                if (k == R.box_a) {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) bg[c] = S[k][c];
+            add_moments<L>(bg, yc, -1.0);
+            lrx_solve<L>(P, R, bg, R.n_a, yc, r, col, o, lin);
+        }
+        if constexpr (NBOX >= 2) {
+            if (P.has_dual) {
+                DualStats<L> D;
+                dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, D);
+                for (int q = 0; q < P.nreq; ++q) {
+                    const ReqDev& R = s_req[q];
+                    if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, R, D, r, col, o, lin);
+                    else if (R.algo == HSAD_DWEST) dwest_solve<L>(R, D, o);
                 }
+            }
+        }
+        return;
+    }
+    for (int q = 0; q < P.nreq; ++q) {
+        const ReqDev& R = s_req[q];
+        if (R.algo == HSAD_LRX) {
+            double bg[NC];
+            select_box<L, NBOX>(S, R.box_a, bg);
             if (R.box_b < 0) {
                 add_moments<L>(bg, yc, -1.0);
             } else {
+                double g[NC];
+                select_box<L, NBOX>(S, R.box_b, g);
 #pragma unroll
-                for (int k = 0; k < NBOX; ++k)
-                    if (k == R.box_b) {
-#pragma unroll
-                        for (int c = 0; c < NC; ++c) bg[c] -= S[k][c];
-                    }
+                for (int c = 0; c < NC; ++c) bg[c] -= g[c];
             }
-            double mu[L], cm[L][L], dv[L];
-            mean_cov<L>(bg, R.n_a, mu, cm);
-            double dmax = 0.0;
-#pragma unroll
-            for (int i = 0; i < L; ++i) {
-                dv[i] = yc[i] - mu[i];
-                dmax = fmax(dmax, fabs(dv[i]));
-            }
-            double score = 0.0;
-            if (dmax > 0.0) {
-                double delta = 0.0;
-                const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
-                if (lin == P.diag_lin) *P.diag_out = delta;
-                if (code) {
-                    report(P, r, col, code);
-                    score = 0.0;
-                }
-            }
-            store_score(R, o, fmax(score, 0.0));
+            lrx_solve<L>(P, R, bg, R.n_a, yc, r, col, o, lin);
         } else {
-            double sin_[NC], sann[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                sin_[c] = 0.0;
-                sann[c] = 0.0;
-            }
-#pragma unroll
-            for (int k = 0; k < NBOX; ++k) {
-                if (k == R.box_b) {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) sin_[c] = S[k][c];
-                }
-                if (k == R.box_a) {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) sann[c] = S[k][c];
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < NC; ++c) sann[c] -= sin_[c];
-            double mu_in[L], mu_out[L], c_out[L][L], md[L];
-            double c_in[L][L];
-            mean_cov<L>(sin_, R.n_a, mu_in, c_in);
-            mean_cov<L>(sann, R.n_b, mu_out, c_out);
-            double mmax = 0.0;
-#pragma unroll
-            for (int i = 0; i < L; ++i) {
-                md[i] = mu_in[i] - mu_out[i];
-                mmax = fmax(mmax, fabs(md[i]));
-            }
-            if (R.algo == HSAD_DWRX) {
-                // detect.cpp:204-223
-                double score = 0.0;
-                if (mmax > 0.0) {
-                    double delta = 0.0;
-                    const int code = chol_quad<L>(c_out, md, R.ridge, score, delta);
-                    if (lin == P.diag_lin) *P.diag_out = delta;
-                    if (code) {
-                        report(P, r, col, code);
-                        score = 0.0;
-                    }
-                }
-                store_score(R, o, fabs(score));
-            } else {
-                // detect.cpp:242-271
-                double cd[L][L], vec[L][L], w[L];
-#pragma unroll
-                for (int i = 0; i < L; ++i)
-#pragma unroll
-                    for (int j = 0; j < L; ++j) cd[i][j] = c_in[i][j] - c_out[i][j];
-                dwest_eigen<L>(cd, vec, w);
-                // detect.cpp:255-263: with eigenvalues sorted descending the loop sums
-                // v_i . m_diff while lambda_i > 0 && lambda_i >= f lambda0 and stops at
-                // the first failure. The condition is monotone in lambda_i, so the summed
-                // set is exactly {i : lambda_i > 0, lambda_i >= f lambda0}: no sort needed.
-                // Sign rule (stats.cpp:83-85): flip v_i so that its first largest-|.|
-                // component is positive.
-                double lmax = w[0];
-#pragma unroll
-                for (int i = 1; i < L; ++i) lmax = fmax(lmax, w[i]);
-                double score = 0.0;
-                int count = 0;
-                if (lmax > 0.0) {
-                    const double cut = R.frac * lmax;
-                    double proj = 0.0;
-#pragma unroll
-                    for (int i = 0; i < L; ++i) {
-                        double best = fabs(vec[0][i]), lead = vec[0][i], dot = vec[0][i] * md[0];
-#pragma unroll
-                        for (int k = 1; k < L; ++k) {
-                            const double av = fabs(vec[k][i]);
-                            lead = av > best ? vec[k][i] : lead;
-                            best = fmax(best, av);
-                            dot = fma(vec[k][i], md[k], dot);
-                        }
-                        const bool take = w[i] > 0.0 && !(w[i] < cut);
-                        proj += take ? (lead < 0.0 ? -dot : dot) : 0.0;
-                        count += take ? 1 : 0;
-                    }
-                    score = fabs(proj);
-                }
-                store_score(R, o, score);
-                if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
-            }
+            double s_in[NC], s_box[NC];
+            select_box<L, NBOX>(S, R.box_b, s_in);
+            select_box<L, NBOX>(S, R.box_a, s_box);
+            DualStats<L> D;
+            dual_stats<L>(s_in, s_box, R.n_a, R.n_b, D);
+            if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, R, D, r, col, o, lin);
+            else dwest_solve<L>(R, D, o);
         }
     }
 }
@@ -593,9 +654,11 @@ __global__ void __launch_bounds__(128, (L <= 5 ? 4 : 1)) detect_kernel(const Det
     constexpr int NC2 = Dim<L>::NC2;
     constexpr int S2 = Dim<L>::S2;
     extern __shared__ double2 s_v2[];
+    __shared__ ReqDev s_req[kMaxRequests];
 
     const int t = threadIdx.x;
     const int NT = blockDim.x;
+    if (t < P.nreq) s_req[t] = P.req[t];  // dynamic request index -> shared memory
     const int ncol = P.tw + 2 * P.rmax;            // strip columns incl. halo
     // pairs per box: S2 (odd) per column + one pad pair per K columns when K > 1,
     // so a thread-to-thread stride of K*S2 + 1 pairs stays odd (conflict-free LDS.128)
@@ -716,7 +779,7 @@ __global__ void __launch_bounds__(128, (L <= 5 ? 4 : 1)) detect_kernel(const Det
                 }
                 double yc[L];
                 shifted(colbase_of(P.rmax + sc), r, yc);
-                solve_pixel<L, NBOX>(P, S, yc, r, col);
+                solve_pixel<L, NBOX>(P, s_req, S, yc, r, col);
             }
         }
         __syncthreads();
@@ -845,6 +908,22 @@ hsad_status plan_requests(const hsad_detect_request* reqs, int n, Plan& plan) {
         d.eigcount = r.algorithm == HSAD_DWEST ? r.d_eigcount : nullptr;
         if (r.score_bytes != 4 && r.score_bytes != 8)
             return set_error(HSAD_E_INVALID_VALUE, "score_bytes must be 4 or 8");
+    }
+    // standard layout: every LRX uses box 0 with the centre excluded and every dual
+    // request uses (outer, inner) = (box 0, box 1) -> select-free solves in the kernel
+    P.std_layout = 1;
+    P.has_dual = 0;
+    P.n_in = P.n_ann = 0.0;
+    for (int q = 0; q < n; ++q) {
+        const ReqDev& d = P.req[q];
+        if (d.algo == HSAD_LRX) {
+            if (d.box_a != 0 || d.box_b != -1) P.std_layout = 0;
+        } else {
+            if (d.box_a != 0 || d.box_b != 1) P.std_layout = 0;
+            P.has_dual = 1;
+            P.n_in = d.n_a;
+            P.n_ann = d.n_b;
+        }
     }
     P.rmax = 0;
     for (int k = 0; k < P.nbox; ++k) P.rmax = P.radius[k] > P.rmax ? P.radius[k] : P.rmax;
