@@ -157,6 +157,16 @@ __device__ __forceinline__ double fast_rcp(double x) {
     return fma(y, e, y);
 }
 
+// fp64 reciprocal square root: MUFU seed + two Newton steps (~1 ulp); CUDA's
+// rsqrt(double) adds special-case handling this code never needs (x > 0 finite).
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
+}
+
 // mean and covariance (divisor N) from box sums: C = S2/N - mu mu^T
 // (== stats.cpp:13-29 in exact arithmetic on the shifted values)
 template <int L>
@@ -201,7 +211,7 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
         ok = ok && (p > 0.0);
         dmax = fmax(dmax, fabs(p));
         dmin = fmin(dmin, p);
-        const double rinv = rsqrt(fmax(p, DBL_MIN));
+        const double rinv = fast_rsqrt(fmax(p, DBL_MIN));
 #pragma unroll
         for (int i = j + 1; i < L; ++i) {
             double v = a[i][j];
@@ -279,7 +289,7 @@ __device__ __forceinline__ double jacobi_t64(double app, double aqq, double apq)
     const double h = aqq - app;
     const double th = 0.5 * h * fast_rcp(apq);
     const double r = fma(th, th, 1.0);
-    double t = fast_rcp(fabs(th) + r * rsqrt(r));
+    double t = fast_rcp(fabs(th) + r * fast_rsqrt(r));
     t = th < 0.0 ? -t : t;
     return apq == 0.0 ? 0.0 : t;
 }
@@ -341,7 +351,7 @@ __device__ __forceinline__ void sweep64(double (&a)[L][L], double (&v)[L][L]) {
         } else {
             t = small ? (apq == 0.0 ? 0.0 : apq * fast_rcp(h)) : jacobi_t64(a[p][p], a[q][q], apq);
             if (small) t = t * fma(-t, t, 1.0);
-            c = rsqrt(fma(t, t, 1.0));
+            c = fast_rsqrt(fma(t, t, 1.0));
         }
         rotate_tc<L, double>(a, v, p, q, t, c);
     }
@@ -389,7 +399,7 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
         double nrm = 0.0;
 #pragma unroll
         for (int k = 0; k < L; ++k) nrm = fma(V[k][j], V[k][j], nrm);
-        const double r = rsqrt(nrm);
+        const double r = fast_rsqrt(nrm);
 #pragma unroll
         for (int k = 0; k < L; ++k) V[k][j] *= r;
     }
@@ -417,12 +427,12 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
             for (int k = 0; k < L; ++k) acc = fma(V[k][i], AV[k][j], acc);
             B[i][j] = acc;
         }
-    // at least two polish sweeps; more (warp-uniform) until the off-diagonal mass
-    // is below (1e-15 |B|)^2 — larger matrices leave fp32 less converged
+    // polish sweeps (warp-uniform) until the off-diagonal mass is below
+    // (1e-15 |B|)^2; larger matrices leave fp32 less converged and need more
 #pragma unroll 1
     for (int sweep = 0; sweep < 8; ++sweep) {
         sweep64<L>(B, V);
-        if (sweep >= 1) {
+        {
             double off = 0.0, dia = 0.0;
 #pragma unroll
             for (int i = 0; i < L; ++i) {
@@ -649,7 +659,10 @@ template <int L, int NBOX, int K>
 // 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
 // fp64 operations, and extra warps hide their latency better than the registers
 // a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
-__global__ void __launch_bounds__(128, (L <= 5 ? 4 : 1)) detect_kernel(const DetectParams P) {
+#ifndef HSAD_DET_MINB
+#define HSAD_DET_MINB 4
+#endif
+__global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kernel(const DetectParams P) {
     constexpr int NC = Dim<L>::NC;
     constexpr int NC2 = Dim<L>::NC2;
     constexpr int S2 = Dim<L>::S2;
