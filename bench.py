@@ -345,6 +345,14 @@ def run_b200(args, cfg, rank, world, local, dist):
     local_px = (r1 - r0) * samples
     red_gbs = nb * samples * (bands * 4 + 32) / (red_ms / 1e3) / 1e9
     step_gbs = value * 1e6 * bpp / 1e9
+    # DRAM traffic per launch from the committed ncu --set full capture of this workload
+    traffic, traffic_src = None, None
+    tfile = ROOT / "profiles" / "ncu_traffic_r1.json"
+    if args.config == "C5" and world == 1 and tfile.exists():
+        tj = json.loads(tfile.read_text())
+        traffic = sum(tj[k]["dram_read_bytes"] + tj[k]["dram_write_bytes"]
+                      for k in ("reduce_bulk_kernel", "detect_kernel")) / 1e9
+        traffic_src = f"GB per step (reduce + detect launches), {tj['source']}"
     line = {
         "metric": "Mpixels/sec for DWT+LRX/DWRX/DWEST scoring",
         "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
@@ -354,7 +362,8 @@ def run_b200(args, cfg, rank, world, local, dist):
                        row_quantum=q, strip_rows=per),
         "roofline": {
             "bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
-            "frac": step_gbs / peak, "traffic": None,
+            "frac": step_gbs / peak, "traffic": traffic, "traffic_unit": traffic_src,
+            "algorithmic_gb_per_step": bpp * total_px / 1e9 / world,
             "basis": f"whole step, algorithmic {bpp} B/px (4L fp32 read + 3 fp64 maps + int8 "
                      f"count) x px/s, {peak_src}",
             "kernels": {

@@ -274,24 +274,28 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Jacobi angle: t = tan(phi) of the rotation zeroing a_pq, written as
+//   t = 2 a_pq sgn(h) / (|h| + sqrt(h^2 + 4 a_pq^2)),  h = a_qq - a_pp
+// (the tan-half-angle form without the a_pq / h quotient): one rsqrt and one
+// reciprocal, and a_pq == 0 gives t = 0 (identity rotation) directly. Only h = a_pq = 0
+// makes the denominator vanish; that case is selected to t = 0.
 __device__ __forceinline__ float jacobi_t32(float app, float aqq, float apq) {
-    const float th = 0.5f * (aqq - app) * rcp_approx(apq);
-    const float ath = fabsf(th);
-    const float r = fmaf(th, th, 1.0f);
-    // |th| > 1e15: th^2 overflows; t -> 1/(2|th|). rcp.approx(inf) = 0 covers a_pq == 0.
-    float t = ath > 1e15f ? 0.5f * rcp_approx(ath) : rcp_approx(ath + r * rsqrtf(r));
-    t = th < 0.0f ? -t : t;
-    return apq == 0.0f ? 0.0f : t;
+    const float h = aqq - app;
+    const float r2 = fmaf(4.0f * apq, apq, h * h);
+    const float den = fabsf(h) + r2 * rsqrtf(r2);
+    float t = 2.0f * apq * rcp_approx(den);
+    t = h < 0.0f ? -t : t;
+    return den > 0.0f ? t : 0.0f;
 }
 
-// fp64 Jacobi angle, general case (fast rcp/rsqrt, ~1 ulp)
+// fp64 general-path angle (fast rcp/rsqrt, ~1 ulp)
 __device__ __forceinline__ double jacobi_t64(double app, double aqq, double apq) {
     const double h = aqq - app;
-    const double th = 0.5 * h * fast_rcp(apq);
-    const double r = fma(th, th, 1.0);
-    double t = fast_rcp(fabs(th) + r * fast_rsqrt(r));
-    t = th < 0.0 ? -t : t;
-    return apq == 0.0 ? 0.0 : t;
+    const double r2 = fma(4.0 * apq, apq, h * h);
+    const double den = fabs(h) + r2 * fast_rsqrt(r2);
+    double t = 2.0 * apq * fast_rcp(den);
+    t = h < 0.0 ? -t : t;
+    return den > 0.0 ? t : 0.0;
 }
 
 // Pairs of one sweep; for L = 4 in parallel order (rounds of two disjoint pairs
