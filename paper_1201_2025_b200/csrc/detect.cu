@@ -168,7 +168,8 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
 }
 
 // mean and covariance (divisor N) from box sums: C = S2/N - mu mu^T
-// (== stats.cpp:13-29 in exact arithmetic on the shifted values)
+// (== stats.cpp:13-29 in exact arithmetic on the shifted values). Symmetric
+// matrices are stored as their upper triangle only (c[i][j], i <= j).
 template <int L>
 __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n, double (&mu)[L],
                                          double (&c)[L][L]) {
@@ -178,11 +179,7 @@ __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
-        for (int j = i; j < L; ++j) {
-            const double v = fma(-mu[i], mu[j], s[tri<L>(i, j)] * inv);
-            c[i][j] = v;
-            c[j][i] = v;
-        }
+        for (int j = i; j < L; ++j) c[i][j] = fma(-mu[i], mu[j], s[tri<L>(i, j)] * inv);
 }
 
 // regularized_inverse + quadratic form (stats.cpp:31-62, detect.cpp:179-180):
@@ -194,6 +191,7 @@ __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n
 template <int L>
 __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L], double ridge,
                                          double& score, double& delta) {
+    // a: upper triangle of C on entry; overwritten with U (C + delta I = U^T U)
     double tr = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i) tr += a[i][i];
@@ -207,21 +205,21 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
     for (int j = 0; j < L; ++j) {
         double p = a[j][j];
 #pragma unroll
-        for (int k = 0; k < j; ++k) p = fma(-a[j][k], a[j][k], p);
+        for (int k = 0; k < j; ++k) p = fma(-a[k][j], a[k][j], p);
         ok = ok && (p > 0.0);
         dmax = fmax(dmax, fabs(p));
         dmin = fmin(dmin, p);
         const double rinv = fast_rsqrt(fmax(p, DBL_MIN));
 #pragma unroll
         for (int i = j + 1; i < L; ++i) {
-            double v = a[i][j];
+            double v = a[j][i];
 #pragma unroll
-            for (int k = 0; k < j; ++k) v = fma(-a[i][k], a[j][k], v);
-            a[i][j] = v * rinv;
+            for (int k = 0; k < j; ++k) v = fma(-a[k][i], a[k][j], v);
+            a[j][i] = v * rinv;
         }
         double zj = d[j];
 #pragma unroll
-        for (int k = 0; k < j; ++k) zj = fma(-a[j][k], z[k], zj);
+        for (int k = 0; k < j; ++k) zj = fma(-a[k][j], z[k], zj);
         z[j] = zj * rinv;
     }
     if (!ok || !(dmax > 0.0) || dmin <= dmax * 1e-14) return HSAD_E_SINGULAR_AFTER_RIDGE;
@@ -232,6 +230,7 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
     score = s;
     return 0;
 }
+
 
 // Symmetric L x L matrices are kept as their upper triangle only (a[i][j], i <= j);
 // sym(a, i, j) addresses element (i, j) for any order with compile-time indices,
@@ -407,30 +406,26 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
 #pragma unroll
         for (int k = 0; k < L; ++k) V[k][j] *= r;
     }
-    // B = V^T A V (upper triangle), A given by its upper triangle
-    double AV[L][L], B[L][L];
+    // B = V^T A V (upper triangle), one column of A V at a time
+    double B[L][L];
 #pragma unroll
-    for (int i = 0; i < L; ++i)
+    for (int j = 0; j < L; ++j) {
+        double w[L];
 #pragma unroll
-        for (int j = 0; j < L; ++j) {
+        for (int i = 0; i < L; ++i) {
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < L; ++k) acc = fma(i <= k ? A[i][k] : A[k][i], V[k][j], acc);
-            AV[i][j] = acc;
+            w[i] = acc;
         }
 #pragma unroll
-    for (int i = 0; i < L; ++i)
-#pragma unroll
-        for (int j = 0; j < L; ++j) {
-            if (j < i) {
-                B[i][j] = 0.0;
-                continue;
-            }
+        for (int i = 0; i <= j; ++i) {
             double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < L; ++k) acc = fma(V[k][i], AV[k][j], acc);
+            for (int k = 0; k < L; ++k) acc = fma(V[k][i], w[k], acc);
             B[i][j] = acc;
         }
+    }
     // polish sweeps (warp-uniform) until the off-diagonal mass is below
     // (1e-15 |B|)^2; larger matrices leave fp32 less converged and need more
 #pragma unroll 1
@@ -488,7 +483,7 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, const ReqDev& R
 // inner-box / annulus statistics shared by DWRX and DWEST (detect.cpp:204-213, 244-253)
 template <int L>
 struct DualStats {
-    double c_in[L][L], c_out[L][L], md[L], mmax;
+    double c_out[L][L], cd[L][L], md[L], mmax;  // upper triangles; cd = C_in - C_ann
 };
 template <int L>
 __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
@@ -498,8 +493,12 @@ __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
     double sann[NC], mu_in[L], mu_out[L];
 #pragma unroll
     for (int c = 0; c < NC; ++c) sann[c] = s_box[c] - s_in[c];
-    mean_cov<L>(s_in, n_in, mu_in, D.c_in);
+    mean_cov<L>(s_in, n_in, mu_in, D.cd);
     mean_cov<L>(sann, n_ann, mu_out, D.c_out);
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) D.cd[i][j] -= D.c_out[i][j];
     D.mmax = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i) {
@@ -519,7 +518,7 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, const ReqDev& 
 #pragma unroll
         for (int i = 0; i < L; ++i)
 #pragma unroll
-            for (int j = 0; j < L; ++j) a[i][j] = D.c_out[i][j];
+            for (int j = i; j < L; ++j) a[i][j] = D.c_out[i][j];
         double delta = 0.0;
         const int code = chol_quad<L>(a, D.md, R.ridge, score, delta);
         if (lin == P.diag_lin) *P.diag_out = delta;
@@ -534,12 +533,8 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, const ReqDev& 
 // DWEST (detect.cpp:242-271)
 template <int L>
 __device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>& D, int64_t o) {
-    double cd[L][L], vec[L][L], w[L];
-#pragma unroll
-    for (int i = 0; i < L; ++i)
-#pragma unroll
-        for (int j = 0; j < L; ++j) cd[i][j] = D.c_in[i][j] - D.c_out[i][j];
-    dwest_eigen<L>(cd, vec, w);
+    double vec[L][L], w[L];
+    dwest_eigen<L>(D.cd, vec, w);
     // With eigenvalues sorted descending the reference loop sums v_i . m_diff while
     // lambda_i > 0 && lambda_i >= f lambda0 and stops at the first failure
     // (detect.cpp:255-262). The condition is monotone in lambda_i, so the summed set
@@ -612,11 +607,10 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
             if (P.has_dual) {
                 DualStats<L> D;
                 dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, D);
-                for (int q = 0; q < P.nreq; ++q) {
-                    const ReqDev& R = s_req[q];
-                    if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, R, D, r, col, o, lin);
-                    else if (R.algo == HSAD_DWEST) dwest_solve<L>(R, D, o);
-                }
+                for (int q = 0; q < P.nreq; ++q)  // DWRX first: C_ann dies before the eigensolve
+                    if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L>(P, s_req[q], D, r, col, o, lin);
+                for (int q = 0; q < P.nreq; ++q)
+                    if (s_req[q].algo == HSAD_DWEST) dwest_solve<L>(s_req[q], D, o);
             }
         }
         return;
