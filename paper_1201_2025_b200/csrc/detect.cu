@@ -32,6 +32,23 @@
 
 #include "hsad_internal.h"
 
+#ifdef HSAD_PHASE_TIMERS
+__device__ unsigned long long g_phase_cycles[8];
+#define PT_START() long long pt_t0 = clock64(); unsigned long long pt_acc[5] = {0, 0, 0, 0, 0}
+#define PT_MARK(i)                                                    \
+    do {                                                              \
+        long long pt_t1 = clock64();                                  \
+        pt_acc[i] += (unsigned long long)(pt_t1 - pt_t0);             \
+        pt_t0 = pt_t1;                                                \
+    } while (0)
+#define PT_FLUSH() \
+    for (int pi = 0; pi < 5; ++pi) atomicAdd(&g_phase_cycles[pi], pt_acc[pi])
+#else
+#define PT_START()
+#define PT_MARK(i)
+#define PT_FLUSH()
+#endif
+
 namespace hsad_b200 {
 
 hsad_status fullband_launch(FbParams& P, cudaStream_t s);
@@ -603,14 +620,24 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
             add_moments<L>(bg, yc, -1.0);
             lrx_solve<L>(P, R, bg, R.n_a, yc, r, col, o, lin);
         }
+#ifdef HSAD_PHASE_TIMERS
+        long long q0 = clock64();  // phases 5/6 sampled on thread 0 of each CTA (x128)
+#endif
         if constexpr (NBOX >= 2) {
             if (P.has_dual) {
                 DualStats<L> D;
                 dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, D);
                 for (int q = 0; q < P.nreq; ++q)  // DWRX first: C_ann dies before the eigensolve
                     if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L>(P, s_req[q], D, r, col, o, lin);
+#ifdef HSAD_PHASE_TIMERS
+                long long q1 = clock64();
+                if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[5], 128ull * (q1 - q0));
+#endif
                 for (int q = 0; q < P.nreq; ++q)
                     if (s_req[q].algo == HSAD_DWEST) dwest_solve<L>(s_req[q], D, o);
+#ifdef HSAD_PHASE_TIMERS
+                if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[6], 128ull * (clock64() - q1));
+#endif
             }
         }
         return;
@@ -725,7 +752,14 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
     }
 
     const int seg0 = t * K;  // first output strip column of this thread (relative to rmax)
+    PT_START();
+    const bool owner1 = K == 1 && seg0 < P.tw && c0 + seg0 < P.samples;
+    const char* own_cb = colbase_of(P.rmax + seg0);
     for (int64_t r = ra; r < rb; ++r) {
+        // K = 1: fetch the centre spectrum first; its latency hides behind the
+        // vertical update, the barrier and the horizontal sums
+        double yc1[L];
+        if (owner1) shifted(own_cb, r, yc1);
         if (r > ra) {
             for (int c = t; c < ncol; c += NT) {
                 const char* cb = colbase_of(c);
@@ -750,7 +784,9 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
                 }
             }
         }
+        PT_MARK(0);  // vertical update
         __syncthreads();
+        PT_MARK(1);  // barrier A
         if (seg0 < P.tw && c0 + seg0 < P.samples) {
             double S[NBOX][NC];
             // horizontal window of the first column of the segment
@@ -789,12 +825,21 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
                     }
                 }
                 double yc[L];
-                shifted(colbase_of(P.rmax + sc), r, yc);
+                if (K == 1) {
+#pragma unroll
+                    for (int i = 0; i < L; ++i) yc[i] = yc1[i];
+                } else {
+                    shifted(colbase_of(P.rmax + sc), r, yc);
+                }
+                PT_MARK(2);  // horizontal + centre load
                 solve_pixel<L, NBOX>(P, s_req, S, yc, r, col);
+                PT_MARK(3);  // solves
             }
         }
         __syncthreads();
+        PT_MARK(4);  // barrier B
     }
+    PT_FLUSH();
 }
 
 template <int L, int NB>
@@ -1161,6 +1206,16 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
 }  // namespace hsad_b200
 
 using namespace hsad_b200;
+
+#ifdef HSAD_PHASE_TIMERS
+extern "C" void hsad_phase_cycles(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+}
+#endif
 
 extern "C" {
 
