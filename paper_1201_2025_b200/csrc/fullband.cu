@@ -98,14 +98,18 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
     const int excl = P.inner;
     const int N = size * size - excl * excl;
 
+    // element offsets of every window sample (and of the DWRX inner box), once
+    int64_t* base = reinterpret_cast<int64_t*>(col + MP);  // [N + excl^2]
+    const int NI = P.algo == HSAD_DWRX ? excl * excl : 0;
+    for (int k = t; k < N + NI; k += kFbThreads)
+        base[k] = k < N ? sample_base(P, ri, c, k, size, excl) : sample_base(P, ri, c, k - N, excl, 0);
+    __syncthreads();
     // pass 1: means
     for (int b = t; b < MP; b += kFbThreads) {
         double s = 0.0, si = 0.0;
         if (b < L) {
-            for (int k = 0; k < N; ++k) s += ld(P, sample_base(P, ri, c, k, size, excl) + b);
-            if (P.algo == HSAD_DWRX)
-                for (int k = 0; k < excl * excl; ++k)
-                    si += ld(P, sample_base(P, ri, c, k, excl, 0) + b);
+            for (int k = 0; k < N; ++k) s += ld(P, base[k] + b);
+            for (int k = 0; k < NI; ++k) si += ld(P, base[N + k] + b);
         }
         mu[b] = b < L ? s / N : 0.0;
         mu[MP + b] = (b < L && P.algo == HSAD_DWRX) ? si / (excl * excl) : 0.0;
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
             __syncthreads();
             for (int e = t; e < nk * MP; e += kFbThreads) {
                 const int k = e / MP, b = e % MP;
-                xs[e] = b < L ? ld(P, sample_base(P, ri, c, k0 + k, size, excl) + b) - mu[b] : 0.0;
+                xs[e] = b < L ? ld(P, base[k0 + k] + b) - mu[b] : 0.0;
             }
             __syncthreads();
             for (int k = 0; k < nk; ++k) {
@@ -208,35 +212,76 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
     if (lin == P.diag_lin && t == 0) *P.diag_out = delta;
     double score = 0.0;
     if (any_d) {
-        // right-looking Cholesky of the bordered matrix, rows 0..L
-        for (int j = 0; j <= L; ++j) {
-            if (t == 0) {
-                const double p = A[packed(j, j)];
-                if (j < L) {
-                    if (!(p > 0.0)) s_bad = 1;
-                    s_dmax = fmax(s_dmax, fabs(p));
-                    s_dmin = fmin(s_dmin, p);
+        // Blocked right-looking Cholesky of the bordered matrix (rows 0..L; the border
+        // row L is updated like any row and its diagonal ends as the Schur complement).
+        // Per 8-column panel: warp 0 factors the panel warp-synchronously, then every
+        // thread applies the rank-8 update to 4x4 tiles of the trailing lower triangle.
+        constexpr int PB = 8;
+        const int warp = t >> 5, lane = t & 31;
+        for (int j0 = 0; j0 < L; j0 += PB) {
+            const int jend = min(j0 + PB, L);  // panel columns [j0, jend)
+            if (warp == 0) {
+                for (int jj = j0; jj < jend; ++jj) {
+                    const double p = A[packed(jj, jj)];
+                    if (lane == 0) {
+                        if (!(p > 0.0)) s_bad = 1;
+                        s_dmax = fmax(s_dmax, fabs(p));
+                        s_dmin = fmin(s_dmin, p);
+                    }
+                    if (!(p > 0.0)) break;  // warp-uniform (every lane read the same p)
+                    const double rinv = rsqrt(p);
+                    for (int i = jj + 1 + lane; i <= L; i += 32) A[packed(i, jj)] *= rinv;
+                    __syncwarp();
+                    // update the rest of the panel: rows i > jj, columns jj < k < jend, k <= i
+                    for (int i = jj + 1 + lane; i <= L; i += 32) {
+                        const double lij = A[packed(i, jj)];
+                        const int kmax = min(i, jend - 1);
+                        for (int k = jj + 1; k <= kmax; ++k)
+                            A[packed(i, k)] = fma(-lij, A[packed(k, jj)], A[packed(i, k)]);
+                    }
+                    __syncwarp();
                 }
-                s_piv = p;
             }
             __syncthreads();
-            if (s_bad || j == L) break;
-            const double rinv = rsqrt(s_piv);
-            for (int i = j + 1 + t; i <= L; i += kFbThreads) {
-                const double v = A[packed(i, j)] * rinv;
-                A[packed(i, j)] = v;
-                col[i] = v;
-            }
-            __syncthreads();
-            // trailing update: rows i > j, columns j < k <= i; warps over rows, lanes over k
-            const int warp = t >> 5, lane = t & 31;
-            for (int i = j + 1 + warp; i <= L; i += kFbThreads / 32) {
-                const double lij = col[i];
-                double* row = A + packed(i, 0);
-                for (int k = j + 1 + lane; k <= i; k += 32) row[k] = fma(-lij, col[k], row[k]);
+            if (s_bad) break;
+            // trailing update: rows i in [jend, L], columns k in [jend, i]
+            const int n = L + 1 - jend;            // trailing rows
+            const int nb = (n + 3) / 4;            // 4-row blocks
+            const int nblocks = nb * (nb + 1) / 2;
+            const int w = jend - j0;               // panel width
+            for (int blk = t; blk < nblocks; blk += kFbThreads) {
+                int bi = static_cast<int>((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
+                while ((bi + 1) * (bi + 2) / 2 <= blk) ++bi;
+                while (bi * (bi + 1) / 2 > blk) --bi;
+                const int bk = blk - bi * (bi + 1) / 2;
+                const int i0 = jend + 4 * bi, k0 = jend + 4 * bk;
+                double li[4][PB], lk[4][PB];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int q = 0; q < PB; ++q) {
+                        li[a][q] = (i0 + a <= L && q < w) ? A[packed(i0 + a, j0 + q)] : 0.0;
+                        lk[a][q] = (k0 + a <= L && q < w) ? A[packed(k0 + a, j0 + q)] : 0.0;
+                    }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int i = i0 + a;
+                    if (i > L) break;
+#pragma unroll
+                    for (int b2 = 0; b2 < 4; ++b2) {
+                        const int k = k0 + b2;
+                        if (k > i) break;
+                        double acc = A[packed(i, k)];
+#pragma unroll
+                        for (int q = 0; q < PB; ++q) acc = fma(-li[a][q], lk[b2][q], acc);
+                        A[packed(i, k)] = acc;
+                    }
+                }
             }
             __syncthreads();
         }
+        if (t == 0) s_piv = A[packed(L, L)];
+        __syncthreads();
         if (t == 0) {
             const bool singular = s_bad || !(s_dmax > 0.0) || s_dmin <= s_dmax * 1e-14;
             if (singular) {
@@ -270,7 +315,10 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
     P.mp = ((P.bands + 1) + 3) / 4 * 4;
     const int64_t tri = static_cast<int64_t>(P.mp) * (P.mp + 1) / 2;
     int chunk = 32;
-    auto bytes = [&](int ch) { return (tri + static_cast<int64_t>(ch) * P.mp + 3 * P.mp) * 8; };
+    const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;  // >= N + inner^2
+    auto bytes = [&](int ch) {
+        return (tri + static_cast<int64_t>(ch) * P.mp + 3 * P.mp + nsamp) * 8;
+    };
     while (chunk > 4 && bytes(chunk) > 220 * 1024) chunk /= 2;
     if (bytes(chunk) > 227 * 1024)
         return set_error(HSAD_E_UNSUPPORTED, "full-band working set exceeds shared memory");
