@@ -146,10 +146,12 @@ def cpu_baseline(cube_rows_np: np.ndarray, lines: int, rows_total: int, budget_s
         oracle.port.dwrx(red, WINDOWS["inner"], WINDOWS["outer"], 1e-6, workers=cores, rows=(0, n))
         oracle.port.dwest(red, WINDOWS["inner"], WINDOWS["outer"], 0.1, workers=cores, rows=(0, n))
         return time.perf_counter() - t0
-    n = 8
-    dt = run(n)
-    n = int(max(8, min(L - WINDOWS["outer"], n * budget_s / max(dt, 1e-3))))
-    dt = run(n)
+    n, dt = 8, 0.0
+    for _ in range(3):  # grow the sample until it takes ~budget_s (or uses every row)
+        dt = run(n)
+        if dt >= 0.6 * budget_s or n >= L - WINDOWS["outer"]:
+            break
+        n = int(max(8, min(L - WINDOWS["outer"], n * budget_s / max(dt, 1e-3))))
     px = n * cube_rows_np.shape[1]
     return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "port",
             "sample": f"rows 0..{n} of the workload ({px} px; DWT on {min(L, n + WINDOWS['outer'])} rows "
