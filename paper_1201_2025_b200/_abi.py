@@ -33,7 +33,7 @@ EXPORTED = [
     "hsad_abi_version", "hsad_status_name", "hsad_last_error_message", "hsad_get_limits",
     "hsad_device_check", "hsad_mirror_index", "hsad_window_validate", "hsad_daubechies_filters",
     "hsad_reduce", "hsad_detect", "hsad_detect_multi", "hsad_strip_rows", "hsad_row_quantum",
-    "hsad_decode_status", "hsad_pipeline_host",
+    "hsad_decode_status", "hsad_pipeline_host", "hsad_reduce_detect",
 ]
 
 
@@ -80,6 +80,8 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
         "hsad_detect": (I32, [VP, I32, I64, I64, I32, P(Request), P(PixelError), VP]),
         "hsad_detect_multi": (I32, [VP, I32, I64, I64, I32, I64, I64, I64, I64, P(Request), I32,
                                     VP, P(PixelError), VP]),
+        "hsad_reduce_detect": (I32, [VP, I64, I64, I32, I32, I32, I64, I64, I64, I64, VP,
+                                     P(Request), I32, VP, P(PixelError), VP]),
         "hsad_strip_rows": (I32, [I64, I64, I64, P(Request), I32, P(I64), P(I64)]),
         "hsad_row_quantum": (I64, [I64, I64]),
         "hsad_decode_status": (I32, [C.c_uint64, I64, P(PixelError)]),

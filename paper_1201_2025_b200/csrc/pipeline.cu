@@ -10,12 +10,6 @@
 
 namespace hsad_b200 {
 
-hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
-                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
-                              int64_t row_begin, int64_t row_end,
-                              const hsad_detect_request* requests, int32_t n_requests,
-                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s);
-
 namespace {
 
 struct DevBuf {
@@ -51,11 +45,6 @@ thread_local PipelineCache g_cache;
 
 using namespace hsad_b200;
 
-extern "C" hsad_status hsad_reduce(const void* d_cube, int32_t elem_bytes, int64_t lines,
-                                   int64_t samples, int32_t bands, int32_t order,
-                                   int32_t target_bands, void* d_out, int32_t out_bytes,
-                                   void* stream);
-
 extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, int64_t samples,
                                           int32_t bands, int32_t order, int32_t target_bands,
                                           const hsad_detect_request* host_requests,
@@ -77,11 +66,13 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
     if (cube_bytes) HSAD_CUDA_TRY(cudaMemcpyAsync(c.cube.p, h_cube, cube_bytes, cudaMemcpyHostToDevice, s));
     const void* d_det = c.cube.p;
     int32_t det_elem = 4;
+    FuseSrc fuse{static_cast<const float*>(c.cube.p), bands, order, nullptr};
     if (order > 0) {
         HSAD_CUDA_TRY(c.reduced.reserve(static_cast<size_t>(npix) * target_bands * sizeof(double)));
-        hsad_status st = hsad_reduce(c.cube.p, 4, lines, samples, bands, order, target_bands,
-                                     c.reduced.p, 8, s);
-        if (st != HSAD_OK) return st;
+        if (npix) {
+            hsad_status st = device_wavelet_map(bands, order, target_bands, &fuse.wmap);
+            if (st != HSAD_OK) return st;
+        }
         d_det = c.reduced.p;
         det_elem = 8;
     }
@@ -98,8 +89,10 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
             dev_req[q].d_eigcount = nullptr;
         }
     }
+    // order > 0: the DWT runs inside the detector launch (or K1 first, see detect.cu)
     hsad_status st = detect_multi_impl(d_det, det_elem, lines, samples, det_bands, 0, lines, 0,
-                                       lines, dev_req, n_requests, nullptr, err, s);
+                                       lines, dev_req, n_requests, nullptr, err, s,
+                                       order > 0 ? &fuse : nullptr);
     if (st != HSAD_OK) return st;
     for (int q = 0; q < n_requests; ++q) {
         const int sb = host_requests[q].score_bytes;

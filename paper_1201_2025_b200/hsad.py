@@ -226,6 +226,48 @@ def detect_multi(cube: torch.Tensor, requests: Sequence[DetectRequest], *, lines
     return outputs
 
 
+def reduce_detect(cube: torch.Tensor, requests: Sequence[DetectRequest],
+                  filters: WaveletFilterPair | int = 2, target_bands: int = 4, *,
+                  lines: int | None = None, buf_row0: int = 0, row_begin: int | None = None,
+                  row_end: int | None = None, status: torch.Tensor | None = None,
+                  reduced: torch.Tensor | None = None, outputs=None):
+    """hsad_reduce_detect: reduce_cube followed by detect_multi in one launch.
+
+    `cube` is the fp32 full-band cube (rows [buf_row0, buf_row0 + cube.shape[0]) of an
+    image with `lines` rows). Returns (reduced, outputs): the fp64 reduced cube of the
+    same rows and the per-request (scores, eigcount-or-None) list of detect_multi.
+    """
+    cube = _require_cuda(cube, "cube")
+    if cube.dtype != torch.float32:
+        raise HsadError(_abi.HSAD_E_INVALID_VALUE, "InvalidValue: reduce_detect takes an fp32 cube")
+    cube = cube.contiguous()
+    order = filters.order if isinstance(filters, WaveletFilterPair) else int(filters)
+    buf_rows, samples, bands = cube.shape
+    lines = buf_rows if lines is None else lines
+    rb = 0 if row_begin is None else row_begin
+    re = lines if row_end is None else row_end
+    if reduced is None:
+        reduced = torch.empty((buf_rows, samples, max(target_bands, 0)), dtype=torch.float64,
+                              device=cube.device)
+    if outputs is None:
+        outputs = []
+        for r in requests:
+            sc = torch.empty((max(re - rb, 0), samples), dtype=r.score_dtype, device=cube.device)
+            cnt = (torch.empty((max(re - rb, 0), samples), dtype=torch.int8, device=cube.device)
+                   if (r.eigcount and r.algorithm == "dwest") else None)
+            outputs.append((sc, cnt))
+    reqs = (Request * len(requests))(*[
+        _make_request(r, sc, cnt) for r, (sc, cnt) in zip(requests, outputs)])
+    err = PixelError()
+    st = _abi.lib().hsad_reduce_detect(cube.data_ptr(), lines, samples, bands, order, target_bands,
+                                       buf_row0, buf_rows, rb, re, reduced.data_ptr(), reqs,
+                                       len(requests),
+                                       status.data_ptr() if status is not None else None,
+                                       C.byref(err), _stream_ptr())
+    _check(st, err)
+    return reduced, outputs
+
+
 def _single(cube: torch.Tensor, algorithm: str, window: WindowConfig, ridge: float,
             eigen_fraction: float, guard: int = 1, score_dtype=torch.float64) -> ScoreMap:
     cube = _require_cuda(cube, "cube")

@@ -36,3 +36,17 @@ for name in sys.argv[1:] or ["C4", "C5"]:
         td = timeit(lambda: hs.detect_multi(red, reqs, status=st, outputs=outs))
         print(f"{name} detect {label} ms {td:.3f}  Mpix/s {npx/td/1e3:.0f}", flush=True)
     del cube, red; torch.cuda.empty_cache()
+    if cfg["bands"] % 16 == 0:
+        cube = generate_rows(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], 0, cfg["lines"], cfg["rate"], device="cuda")
+        reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwrx", W2(5, 11)),
+                hs.DetectRequest("dwest", W2(5, 11), eigcount=True)]
+        st = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        red, outs = hs.reduce_detect(cube, reqs, status=st)
+        tf = timeit(lambda: hs.reduce_detect(cube, reqs, status=st, reduced=red, outputs=outs))
+        print(f"{name} FUSED reduce+detect all3 ms {tf:.3f}  Mpix/s {npx/tf/1e3:.0f}", flush=True)
+        import os
+        for env in ("HSAD_FUSED_DWT_ONLY", "HSAD_NO_FUSE"):
+            os.environ[env] = "1"
+            tf = timeit(lambda: hs.reduce_detect(cube, reqs, status=st, reduced=red, outputs=outs))
+            print(f"{name} {env} ms {tf:.3f}", flush=True)
+            del os.environ[env]

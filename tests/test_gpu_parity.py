@@ -403,3 +403,141 @@ def test_fullband_dwest_unsupported_and_errors(orc):
     with pytest.raises(hs.HsadError) as got:
         hs.local_rx(gpu(flat), W1(3), 1e-6)
     assert str(got.value) == str(want.value)
+
+
+# ------------------------------------------------------------------ fused reduce + detect
+ALL3 = [("lrx", W1(11), {}), ("dwrx", W2(5, 11), {}), ("dwest", W2(5, 11), {})]
+
+
+def _fused_vs_oracle(orc, cube_np, reqs_spec, order=2, what=""):
+    """hsad_reduce_detect against the oracle's reduce_cube + detectors."""
+    cube = gpu(cube_np.astype(np.float32))
+    reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in reqs_spec]
+    red, outs = hs.reduce_detect(cube, reqs, order, 4)
+    torch.cuda.synchronize()
+    red_o = orc.port.reduce_cube(host(cube).astype(np.float64), order, 4, workers=8)
+    assert max_rel_diff(host(red), red_o) < 1e-12, what
+    for (a, w, kw), (s, c) in zip(reqs_spec, outs):
+        s = host(s)
+        if a == "lrx":
+            want = orc.port.local_rx(red_o, w.single_size, 1e-6, guard=kw.get("guard", 1), workers=8)
+        elif a == "dwrx":
+            want = orc.port.dwrx(red_o, w.inner_size, w.outer_size, 1e-6, workers=8)
+        else:
+            want, wc = orc.port.dwest(red_o, w.inner_size, w.outer_size, 0.1, workers=8)
+            assert np.array_equal(host(c), wc), f"{what} {a} eigen-counts"
+        assert max_rel_diff(s, want) < TOL64, f"{what} {a}"
+    return red, outs
+
+
+def test_reduce_detect_config_c4(orc):
+    cfg = CONFIGS["C4"]
+    cube, truth = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"],
+                                 cfg["rate"], device=DEV)
+    _, outs = _fused_vs_oracle(orc, host(cube), ALL3, what="C4")
+    # the fused launch and the two-step path agree to DWT rounding
+    reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in ALL3]
+    two = hs.detect_multi(hs.reduce_cube(cube, 2, 4), reqs)
+    for (a, b), (c, d) in zip(outs, two):
+        assert max_rel_diff(host(a), host(c)) < 1e-9
+        if b is not None:
+            assert torch.equal(b, d)
+
+
+@pytest.mark.parametrize("lines,samples,bands,spec", [
+    (203, 300, 64, ALL3),                                           # ragged last chunk / strip
+    (37, 1100, 32, [("dwrx", W2(3, 9), {}), ("dwest", W2(3, 9), {})]),  # 2-column segments
+    (40, 2100, 16, [("lrx", W1(7), {})]),                           # 4-column segments, 1 box
+    (9, 9, 48, [("lrx", W1(5), {}), ("dwrx", W2(1, 5), {})]),         # tiny image
+])
+def test_reduce_detect_shapes(orc, lines, samples, bands, spec):
+    cube = orc.port.random_cube(lines, samples, bands, 4242 + bands)
+    _fused_vs_oracle(orc, cube, spec, what=f"{lines}x{samples}x{bands}")
+
+
+def test_reduce_detect_strip_bit_identical(orc):
+    lines, samples = 230, 400
+    cube = gpu(orc.port.random_cube(lines, samples, 32, 91).astype(np.float32))
+    reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwrx", W2(5, 11)),
+            hs.DetectRequest("dwest", W2(5, 11), eigcount=True)]
+    red_w, whole = hs.reduce_detect(cube, reqs)
+    q = hs.row_quantum(lines, samples)
+    for g in (2, 3, 8):
+        per = -(-lines // (g * q)) * q
+        for r0 in range(0, lines, per):
+            r1 = min(lines, r0 + per)
+            b0, nb = hs.strip_rows(lines, r0, r1, reqs)
+            red, part = hs.reduce_detect(cube[b0:b0 + nb], reqs, lines=lines, buf_row0=b0,
+                                         row_begin=r0, row_end=r1)
+            assert torch.equal(red, red_w[b0:b0 + nb])
+            for (ws, wc), (ps, pc) in zip(whole, part):
+                assert torch.equal(ws[r0:r1], ps)
+                if wc is not None:
+                    assert torch.equal(wc[r0:r1], pc)
+
+
+@pytest.mark.parametrize("bands,target,spec", [
+    (189, 4, ALL3),                              # bands not a multiple of 16: K1 first
+    (64, 8, [("dwrx", W2(3, 7), {})]),           # 8 reduced bands: K1 first
+    (64, 4, [("lrx", W1(25), {})]),              # window reaches past one chunk: K1 first
+    (64, 4, [("lrx", W1(3), {}), ("lrx", W1(3), {"guard": 1}), ("dwrx", W2(5, 9), {}),
+             ("dwrx", W2(3, 7), {})]),           # 4 window sizes: K1 first
+])
+def test_reduce_detect_fallback_equals_two_step(orc, bands, target, spec):
+    cube = gpu(orc.port.random_cube(60, 70, bands, 5).astype(np.float32))
+    reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in spec]
+    red, outs = hs.reduce_detect(cube, reqs, 2, target)
+    red2 = hs.reduce_cube(cube, 2, target)
+    two = hs.detect_multi(red2, reqs)
+    assert torch.equal(red, red2)
+    for (a, b), (c, d) in zip(outs, two):
+        assert torch.equal(a, c)
+
+
+def test_reduce_detect_env_switch_and_empty(orc, monkeypatch):
+    cube = gpu(orc.port.random_cube(50, 60, 64, 6).astype(np.float32))
+    reqs = [hs.DetectRequest("dwest", W2(3, 7), eigcount=True)]
+    red_f, fused = hs.reduce_detect(cube, reqs)
+    monkeypatch.setenv("HSAD_NO_FUSE", "1")
+    red_t, two = hs.reduce_detect(cube, reqs)
+    monkeypatch.delenv("HSAD_NO_FUSE")
+    assert torch.equal(red_t, hs.reduce_cube(cube, 2, 4))
+    assert max_rel_diff(host(red_f), host(red_t)) < 1e-14
+    assert max_rel_diff(host(fused[0][0]), host(two[0][0])) < 1e-9
+    # nothing to detect: the reduced cube is still produced
+    red_e, outs = hs.reduce_detect(cube, reqs, row_begin=10, row_end=10)
+    assert torch.equal(red_e, red_t) and outs[0][0].numel() == 0
+
+
+def test_reduce_detect_errors(orc):
+    cube = np.zeros((5, 5, 64), dtype=np.float32)
+    cube[2, 2] = 1.0
+    reqs = [hs.DetectRequest("lrx", W1(3))]
+    with pytest.raises(hs.HsadError) as want:
+        hs.detect_multi(hs.reduce_cube(gpu(cube), 2, 4), reqs)
+    with pytest.raises(hs.HsadError) as got:
+        hs.reduce_detect(gpu(cube), reqs)
+    assert (got.value.name, got.value.row, got.value.col) == (want.value.name, want.value.row,
+                                                              want.value.col)
+    assert str(got.value) == str(want.value)
+    for order, target, name in ((0, 4, "UnsupportedOrder"), (2, 3, "InvalidValue"),
+                                (2, 512, "TargetTooLarge")):
+        with pytest.raises(hs.HsadError) as e:
+            hs.reduce_detect(gpu(cube), reqs, order, target)
+        assert e.value.name == name
+    with pytest.raises(hs.HsadError) as e:
+        hs.reduce_detect(gpu(cube), [hs.DetectRequest("lrx", W2(1, 3))])
+    assert e.value.name == "ConfigMismatch"
+
+
+def test_pipeline_host_fused_224(orc):
+    cube = torch.as_tensor(orc.port.random_cube(120, 130, 224, 8).astype(np.float32))
+    reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in ALL3]
+    outs = [(torch.empty((120, 130), dtype=r.score_dtype).pin_memory(),
+             torch.empty((120, 130), dtype=torch.int8) if r.eigcount else None) for r in reqs]
+    hs.pipeline_host(cube.pin_memory(), 2, 4, reqs, outs)
+    _, dev = hs.reduce_detect(cube.to(DEV), reqs)
+    for (a, ac), (b, bc) in zip(outs, dev):
+        assert torch.equal(a, b.cpu())
+        if ac is not None:
+            assert torch.equal(ac, bc.cpu())
