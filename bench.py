@@ -13,7 +13,8 @@ One step = one pass of that hot path over the cube:
           hsad_reduce + hsad_detect_multi (C-ABI) on the launching stream,
           barrier + synchronize on both sides, max over ranks;
   e2e   : hsad_pipeline_host (C-ABI) from pinned HOST memory: H2D of the cube,
-          reduce, detectors, D2H of every map, timed per step.
+          reduce, detectors, D2H of every map, timed per step (row strips on
+          three streams, so the kernels and the D2H overlap the PCIe H2D).
 Multi-GPU (torchrun): row strips aligned to hsad_row_quantum, each rank holds its
 strip + mirror halo (generated from the same seeded row chunks = the host copy),
 computes it, and the fp64 maps are gathered to rank 0 with NCCL (dist.gather)
@@ -329,12 +330,25 @@ def run_b200(args, cfg, rank, world, local, dist):
             hs.pipeline_host(host_cube, 2, 4, reqs, host_out)
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         h2d = nb * samples * bands * 4
+        # PCIe ceiling: one plain pinned H2D copy of the same cube
+        dev_copy = torch.empty_like(host_cube, device=dev)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        dev_copy.copy_(host_cube, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_only_s = time.perf_counter() - t1
+        del dev_copy
         d2h = sum(nb * samples * (8 + (1 if r.eigcount else 0)) for r in reqs)
         e2e = {"value": nb * samples / e2e_s / 1e6, "unit": "Mpixel/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s * 1e3,
-               "path": "hsad_pipeline_host (C-ABI): pinned host cube -> H2D -> reduce -> fused "
-                       "detectors -> D2H" + (f" (rank 0 strip, {nb} rows)" if world > 1 else "")}
+               "h2d_only_ms": h2d_only_s * 1e3,
+               "h2d_gbs": h2d / h2d_only_s / 1e9,
+               "bound": "PCIe: the fp32 cube H2D; reduce, detectors and map D2H run under it "
+                        "in row strips (hsad_pipeline_host)",
+               "path": "hsad_pipeline_host (C-ABI): pinned host cube -> row-strip pipelined "
+                       "H2D / reduce / fused detectors / D2H" +
+                       (f" (rank 0 strip, {nb} rows)" if world > 1 else "")}
 
     if rank != 0:
         return

@@ -17,7 +17,7 @@
  *                               window statistics (the fused B200 path; same per-detector
  *                               semantics as hsad_detect)
  *   hsad_reduce_detect       <- hsad::reduce_cube followed by hsad_detect_multi on the reduced
- *                               cube, in one launch (the DWT runs inside the detector kernel)
+ *                               cube (device buffers, one call)
  *   hsad_pipeline_host       <- hsad::reduce_cube + hsad::detect on HOST buffers, i.e. the
  *                               `hsad reduce` + `hsad detect` CLI composition
  *                               (proj/tools/hsad_main.cpp:112-198) without file I/O
@@ -182,16 +182,13 @@ hsad_status hsad_detect_multi(const void* d_cube, int32_t elem_bytes, int64_t li
                               const hsad_detect_request* requests, int32_t n_requests,
                               uint64_t* d_status, hsad_pixel_error* err, void* stream);
 
-/* reduce_cube + hsad_detect_multi in one call. d_cube (fp32 BIP, `bands` bands) and
- * d_reduced (fp64 BIP, target_bands bands) both hold global rows [buf_row0,
- * buf_row0 + buf_rows); on return d_reduced holds reduce_cube of those rows and the
- * requests' maps hold rows [row_begin, row_end) — the same values as hsad_reduce
- * followed by hsad_detect_multi up to fp64 summation order of the DWT (<= 1e-15
- * relative). Errors: reduction errors (wavelet.cpp:122-167) first, then the
- * detectors' errors exactly as hsad_detect_multi. When target_bands == 4, bands is
- * a multiple of 16 and the windows fit the kernel's neighbourhood, the DWT runs
- * inside the detector launch (one kernel); otherwise hsad_reduce runs first.
- * Asynchrony as hsad_detect_multi (d_status). */
+/* reduce_cube + hsad_detect_multi in one call (the `hsad reduce` + `hsad detect`
+ * composition on device buffers). d_cube (fp32 BIP, `bands` bands) and d_reduced
+ * (fp64 BIP, target_bands bands) both hold global rows [buf_row0, buf_row0 +
+ * buf_rows); on return d_reduced holds reduce_cube of those rows and the requests'
+ * maps hold rows [row_begin, row_end), bit-identical to hsad_reduce followed by
+ * hsad_detect_multi. Reduction errors (wavelet.cpp:122-167) come first, then the
+ * detectors' errors. Asynchrony as hsad_detect_multi (d_status). */
 hsad_status hsad_reduce_detect(const float* d_cube, int64_t lines, int64_t samples, int32_t bands,
                                int32_t order, int32_t target_bands, int64_t buf_row0,
                                int64_t buf_rows, int64_t row_begin, int64_t row_end,

@@ -117,7 +117,7 @@ __device__ __forceinline__ int mirror32(int i, int n) {
 }
 
 // y = spectrum at (global row vrow, this thread's data column) as fp64
-template <int L, bool CG = false>
+template <int L>
 __device__ __forceinline__ void load_row(const DetectParams& P, const char* colbase,
                                          int64_t row_bytes, int vrow, double (&y)[L]) {
     const int drow = mirror32(vrow, static_cast<int>(P.lines)) - static_cast<int>(P.buf_row0);
@@ -127,19 +127,18 @@ __device__ __forceinline__ void load_row(const DetectParams& P, const char* colb
         if constexpr (L % 2 == 0) {
 #pragma unroll
             for (int i = 0; i < L; i += 2) {
-                const double2 v = CG ? __ldcg(reinterpret_cast<const double2*>(d + i))
-                                     : __ldg(reinterpret_cast<const double2*>(d + i));
+                const double2 v = __ldg(reinterpret_cast<const double2*>(d + i));
                 y[i] = v.x;
                 y[i + 1] = v.y;
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < L; ++i) y[i] = CG ? __ldcg(d + i) : __ldg(d + i);
+            for (int i = 0; i < L; ++i) y[i] = __ldg(d + i);
         }
     } else {
         const float* f = reinterpret_cast<const float*>(p);
 #pragma unroll
-        for (int i = 0; i < L; ++i) y[i] = static_cast<double>(CG ? __ldcg(f + i) : __ldg(f + i));
+        for (int i = 0; i < L; ++i) y[i] = static_cast<double>(__ldg(f + i));
     }
 }
 
@@ -681,19 +680,23 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
 //   3. barrier before the next row's update.
 // Smem column stride: S2 double2 per column plus one pad pair after every K
 // columns, so the per-thread segments (stride K columns) hit distinct banks.
-// One (strip, row range) unit of the detector: the body of detect_kernel, also
-// called by the fused reduce+detect kernel. CG loads: read the reduced cube through
-// L2 only (it is written earlier in the same launch by the fused kernel).
-template <int L, int NBOX, int K, bool CG>
-__device__ __forceinline__ void detect_unit(const DetectParams& P, const ReqDev* s_req,
-                                            double2* s_v2, int64_t strip, int64_t ra,
-                                            int64_t rb) {
+template <int L, int NBOX, int K>
+// 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
+// fp64 operations, and extra warps hide their latency better than the registers
+// a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
+#ifndef HSAD_DET_MINB
+#define HSAD_DET_MINB 4
+#endif
+__global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kernel(const DetectParams P) {
     constexpr int NC = Dim<L>::NC;
     constexpr int NC2 = Dim<L>::NC2;
     constexpr int S2 = Dim<L>::S2;
+    extern __shared__ double2 s_v2[];
+    __shared__ ReqDev s_req[kMaxRequests];
 
     const int t = threadIdx.x;
     const int NT = blockDim.x;
+    if (t < P.nreq) s_req[t] = P.req[t];  // dynamic request index -> shared memory
     const int ncol = P.tw + 2 * P.rmax;            // strip columns incl. halo
     // pairs per box: S2 (odd) per column + one pad pair per K columns when K > 1,
     // so a thread-to-thread stride of K*S2 + 1 pairs stays odd (conflict-free LDS.128)
@@ -701,7 +704,9 @@ __device__ __forceinline__ void detect_unit(const DetectParams& P, const ReqDev*
     auto vslot = [&](int k, int c) -> double2* {    // c: strip column index 0..ncol-1
         return s_v2 + k * box_stride + c * S2 + (K > 1 ? c / K : 0);
     };
-    const int64_t c0 = strip * P.tw;  // first output column
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P.tw;  // first output column
+    const int64_t ra = P.row_begin + static_cast<int64_t>(blockIdx.y) * P.chunk;
+    const int64_t rb = min(ra + P.chunk, P.row_end);
     if (ra >= rb) return;
     const int64_t row_bytes = P.samples * L * P.elem_bytes;
 
@@ -709,8 +714,8 @@ __device__ __forceinline__ void detect_unit(const DetectParams& P, const ReqDev*
     double shift[L];
     {
         double y[L];
-        load_row<L, CG>(P, static_cast<const char*>(P.cube) + c0 * L * P.elem_bytes, row_bytes,
-                        static_cast<int>(ra), y);
+        load_row<L>(P, static_cast<const char*>(P.cube) + c0 * L * P.elem_bytes, row_bytes,
+                    static_cast<int>(ra), y);
 #pragma unroll
         for (int i = 0; i < L; ++i) shift[i] = y[i];
     }
@@ -720,7 +725,7 @@ __device__ __forceinline__ void detect_unit(const DetectParams& P, const ReqDev*
         return static_cast<const char*>(P.cube) + static_cast<int64_t>(dcol) * L * P.elem_bytes;
     };
     auto shifted = [&](const char* cb, int64_t vrow, double (&y)[L]) {
-        load_row<L, CG>(P, cb, row_bytes, static_cast<int>(vrow), y);
+        load_row<L>(P, cb, row_bytes, static_cast<int>(vrow), y);
 #pragma unroll
         for (int i = 0; i < L; ++i) y[i] -= shift[i];
     };
@@ -837,150 +842,6 @@ __device__ __forceinline__ void detect_unit(const DetectParams& P, const ReqDev*
     PT_FLUSH();
 }
 
-// 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
-// fp64 operations, and extra warps hide their latency better than the registers
-// a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
-#ifndef HSAD_DET_MINB
-#define HSAD_DET_MINB 4
-#endif
-template <int L, int NBOX, int K>
-__global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kernel(const DetectParams P) {
-    extern __shared__ double2 s_v2[];
-    __shared__ ReqDev s_req[kMaxRequests];
-    if (threadIdx.x < P.nreq) s_req[threadIdx.x] = P.req[threadIdx.x];  // dynamic index -> smem
-    const int64_t ra = P.row_begin + static_cast<int64_t>(blockIdx.y) * P.chunk;
-    const int64_t rb = min(ra + P.chunk, P.row_end);
-    detect_unit<L, NBOX, K, false>(P, s_req, s_v2, blockIdx.x, ra, rb);
-}
-
-// ---- fused reduce + detect (K1 folded into the detector stream) -----------------
-// Units are (global chunk c of `chunk` rows, strip s of TW columns) in raster order.
-// A persistent CTA takes ticket v: it reduces DWT unit v (its own pixels only, each
-// pixel once) into the fp64 reduced buffer and publishes flags[v] = epoch (release);
-// then it runs the detector on unit v - lag, lag = strips + 2, after acquiring the
-// flags of the up to 9 units whose reduced rows its windows read (all of them have
-// smaller tickets, held by running CTAs whose DWT step never waits: no deadlock,
-// no co-residency requirement). HBM-bound DWT units interleave with fp64-bound
-// detector units on every SM.
-struct FusedParams {
-    DetectParams D;          // detector params; D.cube = reduced buffer (fp64, 4 bands)
-    const float* full;       // full-band rows [D.buf_row0, D.buf_row0 + D.buf_rows)
-    int full_bands;          // multiple of 16
-    const double* wmap;      // 4 x full_bands
-    unsigned int* flags;     // per DWT unit
-    unsigned int* ticket;    // zeroed per launch
-    unsigned int epoch;
-    int strips;
-    int64_t c_lo, c_hi;      // DWT chunks [c_lo, c_hi)
-    int64_t d_lo, d_hi;      // detector chunks [d_lo, d_hi)
-    int lag;
-};
-
-// DWT of one unit with mma.m8n8k4.f64 (see reduce.cu, reduce_dmma16_kernel):
-// groups of 8 consecutive pixels of a row, 16 bands per float4 load.
-__device__ __forceinline__ void fused_dwt_unit(const FusedParams& F, const double* s_wt,
-                                               int64_t c, int64_t s) {
-    const DetectParams& P = F.D;
-    const int64_t r0 = max(c * P.chunk, P.buf_row0), r1 = min((c + 1) * P.chunk, P.buf_row0 + P.buf_rows);
-    const int64_t x0 = s * P.tw, x1 = min(x0 + P.tw, P.samples);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const int m = lane >> 2, q = lane & 3;
-    const int gpr = static_cast<int>((x1 - x0 + 7) / 8);  // groups per row
-    const int64_t ngroups = (r1 - r0) * gpr;
-    const int nblk = F.full_bands >> 4;  // 16-band blocks per pixel
-    for (int64_t g = warp; g < ngroups; g += nwarp) {
-        const int64_t row = r0 + g / gpr;
-        const int64_t col = x0 + (g % gpr) * 8 + m;
-        const int64_t colc = min(col, x1 - 1);
-        const float4* src = reinterpret_cast<const float4*>(
-                                F.full + ((row - P.buf_row0) * P.samples + colc) * F.full_bands) + q;
-        double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-        // up to 16 independent 16-byte loads (256 bands) in flight per lane before
-        // the first MMA
-        for (int b0 = 0; b0 < nblk; b0 += 16) {
-            float4 x[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-                x[i] = b0 + i < nblk ? __ldcs(src + 4 * (b0 + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (b0 + i >= nblk) break;  // warp-uniform
-                const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
-                const double* wrow = s_wt + ((b0 + i) * 16 + 4 * q) * 5 + m;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const double a = static_cast<double>(xs[j]);
-                    const double b = m < 4 ? wrow[j * 5] : 0.0;
-                    asm volatile(
-                        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                        : "+d"(d[j][0]), "+d"(d[j][1])
-                        : "d"(a), "d"(b));
-                }
-            }
-        }
-        if (q < 2 && col < x1) {
-            const double y0 = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
-            const double y1 = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
-            double2* dst = reinterpret_cast<double2*>(const_cast<void*>(P.cube)) +
-                           ((row - P.buf_row0) * P.samples + col) * 2 + q;
-            __stcg(dst, make_double2(y0, y1));
-        }
-    }
-}
-
-template <int NBOX, int K>
-__global__ void __launch_bounds__(128, 4) fused_kernel(const FusedParams F) {
-    constexpr int L = 4;
-    extern __shared__ double2 s_v2[];
-    __shared__ ReqDev s_req[kMaxRequests];
-    __shared__ unsigned int s_ticket;
-    const DetectParams& P = F.D;
-    const int t = threadIdx.x;
-    if (t < P.nreq) s_req[t] = P.req[t];
-    // W^T for the DWT, after the detector's vertical-sum area
-    const int ncol = P.tw + 2 * P.rmax;
-    double* s_wt = reinterpret_cast<double*>(s_v2 + NBOX * (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)));
-    for (int i = t; i < F.full_bands * 4; i += blockDim.x) {
-        const int n = i / F.full_bands, k = i % F.full_bands;
-        s_wt[k * 5 + n] = F.wmap[i];
-    }
-    const int64_t ndwt = (F.c_hi - F.c_lo) * F.strips;
-    for (;;) {
-        __syncthreads();
-        if (t == 0) s_ticket = atomicAdd(F.ticket, 1u);
-        __syncthreads();
-        const int64_t v = s_ticket;
-        if (v >= ndwt + F.lag) break;
-        if (v < ndwt) {
-            fused_dwt_unit(F, s_wt, F.c_lo + v / F.strips, v % F.strips);
-            __threadfence();
-            __syncthreads();
-            if (t == 0)
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(F.flags + v), "r"(F.epoch)
-                             : "memory");
-        }
-        const int64_t u = v - F.lag;
-        if (u < 0 || u >= ndwt) continue;
-        const int64_t c = F.c_lo + u / F.strips, st = u % F.strips;
-        if (c < F.d_lo || c >= F.d_hi) continue;
-        if (t == 0) {
-            for (int64_t cc = max(c - 1, F.c_lo); cc <= min(c + 1, F.c_hi - 1); ++cc)
-                for (int64_t ss = max(st - 1, int64_t(0)); ss <= min(st + 1, int64_t(F.strips - 1)); ++ss) {
-                    const unsigned int* f = F.flags + (cc - F.c_lo) * F.strips + ss;
-                    unsigned int val;
-                    for (;;) {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(val) : "l"(f) : "memory");
-                        if (val == F.epoch) break;
-                        __nanosleep(100);
-                    }
-                }
-        }
-        __syncthreads();
-        const int64_t ra = max(c * P.chunk, P.row_begin), rb = min((c + 1) * P.chunk, P.row_end);
-        detect_unit<L, NBOX, K, true>(P, s_req, s_v2, st, ra, rb);
-    }
-}
-
 template <int L, int NB>
 cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
     const int ncol = P.tw + 2 * P.rmax;
@@ -1026,40 +887,6 @@ cudaError_t launch_detect(int bands, const DetectParams& P, dim3 grid, int nt, i
         case 8: return launch_l<8>(P, grid, nt, kcols, s);
     }
     return cudaErrorInvalidValue;
-}
-
-template <int NB, int K>
-cudaError_t launch_fused_k(const FusedParams& F, cudaStream_t s) {
-    const int ncol = F.D.tw + 2 * F.D.rmax;
-    const size_t smem =
-        static_cast<size_t>(NB) * (ncol * Dim<4>::S2 + (K > 1 ? ncol / K + 1 : 0)) * sizeof(double2) +
-        static_cast<size_t>(F.full_bands) * 5 * sizeof(double);
-    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    auto kern = fused_kernel<NB, K>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
-    if (e != cudaSuccess) return e;
-    const int64_t tickets = (F.c_hi - F.c_lo) * F.strips + F.lag;
-    int64_t grid = static_cast<int64_t>(sms) * (occ < 1 ? 1 : occ);
-    grid = grid < tickets ? grid : tickets;
-    kern<<<static_cast<unsigned>(grid), 128, smem, s>>>(F);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_fused(const FusedParams& F, int kcols, cudaStream_t s) {
-    if (F.D.nbox == 1) {
-        if (kcols == 4) return launch_fused_k<1, 4>(F, s);
-        if (kcols == 2) return launch_fused_k<1, 2>(F, s);
-        return launch_fused_k<1, 1>(F, s);
-    }
-    if (kcols == 4) return launch_fused_k<2, 4>(F, s);
-    if (kcols == 2) return launch_fused_k<2, 2>(F, s);
-    return launch_fused_k<2, 1>(F, s);
 }
 
 const char* algo_name(int a) {
@@ -1189,19 +1016,7 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                               int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
                               int64_t row_begin, int64_t row_end,
                               const hsad_detect_request* requests, int32_t n_requests,
-                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s,
-                              const FuseSrc* fuse) {
-    // hsad_reduce_detect with nothing to detect still fills the reduced buffer
-    if (fuse && (row_begin >= row_end || samples == 0)) {
-        if (row_begin < 0 || row_end > lines || row_begin > row_end)
-            return set_error(HSAD_E_INVALID_VALUE, "row range outside the image");
-        if (err) {
-            err->code = HSAD_OK;
-            err->row = err->col = -1;
-        }
-        return hsad_reduce(fuse->full, 4, buf_rows, samples, fuse->bands, fuse->order, bands,
-                           const_cast<void*>(d_cube), elem_bytes, s);
-    }
+                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s) {
     if (err) {
         err->code = HSAD_OK;
         err->row = err->col = -1;
@@ -1297,6 +1112,8 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     }
     P.status = status;
+    // diagnostic scratch per request: scores (8 B/px) + eigen-count (1 B/px), 16-byte aligned
+    const size_t scratch_stride = (static_cast<size_t>(samples) * 9 + 15) / 16 * 16;
     // full-band launcher: one fullband_kernel launch per request over rows [rb, re)
     auto launch_fb = [&](int64_t rb, int64_t re, int64_t diag_lin, double* diag_out,
                          char* scratch) -> hsad_status {
@@ -1315,7 +1132,7 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             F.outer = R.algorithm == HSAD_LRX ? R.window.single_size : R.window.outer_size;
             F.inner = R.algorithm == HSAD_LRX ? (R.guard <= 0 ? 1 : R.guard) : R.window.inner_size;
             F.ridge = R.ridge;
-            F.scores = scratch ? static_cast<void*>(scratch + static_cast<size_t>(samples) * 9 * q)
+            F.scores = scratch ? static_cast<void*>(scratch + scratch_stride * q)
                                : R.d_scores;
             F.score_bytes = R.score_bytes;
             F.status = status;
@@ -1327,44 +1144,9 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         return HSAD_OK;
     };
     cudaError_t e = cudaSuccess;
-    // fused reduce + detect: the DWT units run inside the detector launch when the
-    // windows stay within one neighbouring chunk / strip; otherwise K1 runs first
-    const bool fused = fuse && !fullband && bands == 4 && elem_bytes == 8 &&
-                       fuse->bands % 16 == 0 && P.nbox <= 2 && P.rmax < P.chunk &&
-                       P.rmax < P.tw && (reinterpret_cast<uintptr_t>(fuse->full) & 15) == 0 &&
-                       !getenv("HSAD_NO_FUSE");
-    if (fuse && !fused) {
-        st = hsad_reduce(fuse->full, 4, buf_rows, samples, fuse->bands, fuse->order, bands,
-                         const_cast<void*>(d_cube), elem_bytes, s);
-        if (st != HSAD_OK) return st;
-    }
-    unsigned int* sync_flags = nullptr;
     if (fullband) {
         hsad_status fst = launch_fb(row_begin, row_end, -1, nullptr, nullptr);
         if (fst != HSAD_OK) return fst;
-    } else if (fused) {
-        FusedParams F{};
-        F.D = P;
-        F.full = fuse->full;
-        F.full_bands = fuse->bands;
-        F.wmap = fuse->wmap;
-        F.strips = static_cast<int>(strips);
-        F.c_lo = buf_row0 / P.chunk;
-        F.c_hi = (buf_row0 + buf_rows + P.chunk - 1) / P.chunk;
-        F.d_lo = row_begin / P.chunk;
-        F.d_hi = (row_end + P.chunk - 1) / P.chunk;
-        if (getenv("HSAD_FUSED_DWT_ONLY")) F.d_hi = F.d_lo;  // timing probe only
-        F.lag = F.strips + 2;
-        F.epoch = 1;
-        const int64_t nflags = (F.c_hi - F.c_lo) * strips + 1;
-        HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&sync_flags),
-                                      static_cast<size_t>(nflags) * sizeof(unsigned int), s));
-        HSAD_CUDA_TRY(cudaMemsetAsync(sync_flags, 0, static_cast<size_t>(nflags) * sizeof(unsigned int), s));
-        F.flags = sync_flags;
-        F.ticket = sync_flags + nflags - 1;
-        e = launch_fused(F, plan.kcols, s);
-        cudaFreeAsync(sync_flags, s);
-        if (e != cudaSuccess) return cuda_fail(e, "hsad fused reduce+detect kernel launch");
     } else {
         e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
         if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
@@ -1395,13 +1177,13 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             // the diagnostic pass writes into scratch rows, never over the results
             char* scratch = nullptr;
             e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                static_cast<size_t>(samples) * 9 * D.nreq, s);
+                                scratch_stride * D.nreq, s);
             if (e != cudaSuccess) return cuda_fail(e, "hsad detect diagnostics");
             for (int q = 0; q < D.nreq; ++q) {
-                D.req[q].scores = scratch + static_cast<size_t>(samples) * 9 * q;
+                D.req[q].scores = scratch + scratch_stride * q;
                 if (D.req[q].eigcount)
                     D.req[q].eigcount = reinterpret_cast<int8_t*>(
-                        scratch + static_cast<size_t>(samples) * (9 * q + 8));
+                        scratch + scratch_stride * q + static_cast<size_t>(samples) * 8);
             }
             if (fullband) {
                 if (launch_fb(row, row + 1, lin, d_diag, scratch) != HSAD_OK) e = cudaErrorUnknown;
@@ -1492,22 +1274,19 @@ hsad_status hsad_reduce_detect(const float* d_cube, int64_t lines, int64_t sampl
                                double* d_reduced, const hsad_detect_request* requests,
                                int32_t n_requests, uint64_t* d_status, hsad_pixel_error* err,
                                void* stream) {
-    if (lines < 0 || samples < 0) return set_error(HSAD_E_INVALID_VALUE, "negative cube extent");
-    hsad_status st = wavelet_plan(bands, order, target_bands, nullptr);
-    if (st != HSAD_OK) return st;
+    if (err) {
+        err->code = HSAD_OK;
+        err->row = err->col = -1;
+    }
     if (buf_row0 < 0 || buf_rows < 0 || buf_row0 + buf_rows > lines)
         return set_error(HSAD_E_INVALID_VALUE, "buffer rows outside the image");
-    if ((!d_cube || !d_reduced) && buf_rows * samples > 0)
-        return set_error(HSAD_E_INVALID_VALUE, "null buffer");
-    const double* d_map = nullptr;
-    if (buf_rows * samples > 0) {
-        st = device_wavelet_map(bands, order, target_bands, &d_map);
-        if (st != HSAD_OK) return st;
-    }
-    const FuseSrc fuse{d_cube, bands, order, d_map};
+    // reduce_cube errors first (the CLI runs `hsad reduce` before `hsad detect`)
+    hsad_status st = hsad_reduce(d_cube, 4, buf_rows, samples, bands, order, target_bands,
+                                 d_reduced, 8, stream);
+    if (st != HSAD_OK) return st;
     return detect_multi_impl(d_reduced, 8, lines, samples, target_bands, buf_row0, buf_rows,
                              row_begin, row_end, requests, n_requests, d_status, err,
-                             static_cast<cudaStream_t>(stream), &fuse);
+                             static_cast<cudaStream_t>(stream));
 }
 
 hsad_status hsad_detect(const void* d_cube, int32_t elem_bytes, int64_t lines, int64_t samples,

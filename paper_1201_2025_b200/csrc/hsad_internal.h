@@ -61,23 +61,6 @@ struct FbParams {
     int mp;             // bordered dimension L+1 rounded up to a multiple of 4
 };
 
-// Full-band fp32 source of a fused reduce + detect call (hsad_reduce_detect): the
-// detector's 4-band fp64 input is produced by the DWT inside the detector launch.
-struct FuseSrc {
-    const float* full;     // full-band rows, same row range as the reduced buffer
-    int32_t bands;
-    int32_t order;
-    const double* wmap;    // composed 4 x bands map (device)
-};
-
-hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
-                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
-                              int64_t row_begin, int64_t row_end,
-                              const hsad_detect_request* requests, int32_t n_requests,
-                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s,
-                              const FuseSrc* fuse = nullptr);
-hsad_status device_wavelet_map(int32_t bands, int32_t order, int32_t target, const double** d_map);
-
 // Kernel-side limits.
 constexpr int kMaxDetectBands = 8;
 constexpr int kMaxBoxes = 4;

@@ -1,14 +1,34 @@
 // hsad_pipeline_host: reduce_cube + detect on HOST buffers — the composition the
 // reference CLI runs (`hsad reduce` then `hsad detect`, proj/tools/hsad_main.cpp:112-198)
-// minus file I/O. H2D of the fp32 cube, K1 reduction into a device-resident
-// reduced cube, one fused K2-K4 pass for every request, D2H of every map.
-// Device buffers are cached per host thread so repeated calls do not re-allocate.
+// minus file I/O.
+//
+// The cube is streamed in row strips so that PCIe and the kernels overlap:
+//
+//   copy stream   : H2D strip i (fp32 rows [r0, r1))            -> event h[i]
+//   caller stream : wait h[i]; K1 reduce of rows [r0, r1);
+//                   detect the output rows whose windows are now complete
+//                   ([d0, d1), multiples of hsad_row_quantum)    -> event d[i]
+//   D2H stream    : wait d[i]; D2H of those map rows
+//
+// Strip boundaries on the row quantum keep every map bit-identical to a single
+// whole-image hsad_reduce + hsad_detect_multi (the detector's strip property).
+// The step is then bound by the H2D of the fp32 cube (PCIe), with the kernels and
+// the map D2H hidden under it except for the last strip. Device buffers, streams
+// and events are cached per host thread so repeated calls do not re-allocate.
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "hsad_internal.h"
 
 namespace hsad_b200 {
+
+hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
+                              int64_t row_begin, int64_t row_end,
+                              const hsad_detect_request* requests, int32_t n_requests,
+                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s);
+int64_t row_quantum(int64_t lines, int64_t samples);
 
 namespace {
 
@@ -35,8 +55,30 @@ struct DevBuf {
     }
 };
 
+constexpr int kMaxStrips = 16;
+
 struct PipelineCache {
-    DevBuf cube, reduced, out[kMaxRequests], counts[kMaxRequests];
+    DevBuf cube, reduced, out[kMaxRequests], counts[kMaxRequests], status;
+    int device = -1;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_h[kMaxStrips] = {}, ev_d[kMaxStrips] = {}, ev_start = nullptr;
+    cudaError_t init() {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (h2d && device == dev) return cudaSuccess;
+        // a device switch leaks the old handles; they belong to the other device
+        h2d = d2h = nullptr;
+        if ((e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (int i = 0; i < kMaxStrips; ++i) {
+            if ((e = cudaEventCreateWithFlags(&ev_h[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&ev_d[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+        if ((e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming)) != cudaSuccess) return e;
+        device = dev;
+        return cudaSuccess;
+    }
 };
 thread_local PipelineCache g_cache;
 
@@ -45,11 +87,21 @@ thread_local PipelineCache g_cache;
 
 using namespace hsad_b200;
 
+extern "C" hsad_status hsad_reduce(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                                   int64_t samples, int32_t bands, int32_t order,
+                                   int32_t target_bands, void* d_out, int32_t out_bytes,
+                                   void* stream);
+
 extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, int64_t samples,
                                           int32_t bands, int32_t order, int32_t target_bands,
                                           const hsad_detect_request* host_requests,
                                           int32_t n_requests, hsad_pixel_error* err,
                                           void* stream) {
+    if (err) {
+        err->code = HSAD_OK;
+        err->row = err->col = -1;
+    }
+    if (lines < 0 || samples < 0) return set_error(HSAD_E_INVALID_VALUE, "negative cube extent");
     if (!h_cube && lines * samples * bands > 0) return set_error(HSAD_E_INVALID_VALUE, "null cube");
     if (n_requests < 1 || n_requests > kMaxRequests || !host_requests)
         return set_error(HSAD_E_INVALID_VALUE, "between 1 and 4 requests per call");
@@ -61,18 +113,14 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
         if (st != HSAD_OK) return st;
     }
     PipelineCache& c = g_cache;
+    HSAD_CUDA_TRY(c.init());
+    const size_t row_px = static_cast<size_t>(samples);
     const size_t cube_bytes = static_cast<size_t>(npix) * bands * sizeof(float);
     HSAD_CUDA_TRY(c.cube.reserve(cube_bytes));
-    if (cube_bytes) HSAD_CUDA_TRY(cudaMemcpyAsync(c.cube.p, h_cube, cube_bytes, cudaMemcpyHostToDevice, s));
     const void* d_det = c.cube.p;
     int32_t det_elem = 4;
-    FuseSrc fuse{static_cast<const float*>(c.cube.p), bands, order, nullptr};
     if (order > 0) {
         HSAD_CUDA_TRY(c.reduced.reserve(static_cast<size_t>(npix) * target_bands * sizeof(double)));
-        if (npix) {
-            hsad_status st = device_wavelet_map(bands, order, target_bands, &fuse.wmap);
-            if (st != HSAD_OK) return st;
-        }
         d_det = c.reduced.p;
         det_elem = 8;
     }
@@ -89,20 +137,96 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
             dev_req[q].d_eigcount = nullptr;
         }
     }
-    // order > 0: the DWT runs inside the detector launch (or K1 first, see detect.cu)
-    hsad_status st = detect_multi_impl(d_det, det_elem, lines, samples, det_bands, 0, lines, 0,
-                                       lines, dev_req, n_requests, nullptr, err, s,
-                                       order > 0 ? &fuse : nullptr);
-    if (st != HSAD_OK) return st;
+    // request validation before any transfer (an empty range validates only)
+    hsad_status st = detect_multi_impl(d_det, det_elem, lines, samples, det_bands, 0, lines, 0, 0,
+                                       dev_req, n_requests, nullptr, err, s);
+    if (st != HSAD_OK || npix == 0) return st;
+    HSAD_CUDA_TRY(c.status.reserve(sizeof(uint64_t)));
+    uint64_t* d_status = static_cast<uint64_t*>(c.status.p);
+    HSAD_CUDA_TRY(cudaMemsetAsync(d_status, 0xff, sizeof(uint64_t), s));
+
+    int64_t rmax = 0;  // rows a window reaches beyond its pixel
     for (int q = 0; q < n_requests; ++q) {
-        const int sb = host_requests[q].score_bytes;
-        if (npix)
-            HSAD_CUDA_TRY(cudaMemcpyAsync(host_requests[q].d_scores, c.out[q].p,
-                                          static_cast<size_t>(npix) * sb, cudaMemcpyDeviceToHost, s));
-        if (dev_req[q].d_eigcount && npix)
-            HSAD_CUDA_TRY(cudaMemcpyAsync(host_requests[q].d_eigcount, c.counts[q].p,
-                                          static_cast<size_t>(npix), cudaMemcpyDeviceToHost, s));
+        const hsad_window& w = host_requests[q].window;
+        const int64_t r = (w.mode == HSAD_WINDOW_SINGLE ? w.single_size : w.outer_size) / 2;
+        rmax = r > rmax ? r : rmax;
     }
-    HSAD_CUDA_TRY(cudaStreamSynchronize(s));
-    return HSAD_OK;
+    const int64_t quantum = row_quantum(lines, samples);
+    int64_t strip = (lines + kMaxStrips - 1) / kMaxStrips;
+    strip = (strip + quantum - 1) / quantum * quantum;
+    if (strip < quantum) strip = quantum;
+
+    // the copy streams start after the caller's earlier work on `stream`
+    HSAD_CUDA_TRY(cudaEventRecord(c.ev_start, s));
+    HSAD_CUDA_TRY(cudaStreamWaitEvent(c.h2d, c.ev_start, 0));
+    HSAD_CUDA_TRY(cudaStreamWaitEvent(c.d2h, c.ev_start, 0));
+    int64_t d_done = 0;
+    int i = 0;
+    for (int64_t r0 = 0; r0 < lines; r0 += strip, ++i) {
+        const int64_t r1 = r0 + strip < lines ? r0 + strip : lines;
+        const size_t off = static_cast<size_t>(r0) * row_px * bands;
+        HSAD_CUDA_TRY(cudaMemcpyAsync(static_cast<float*>(c.cube.p) + off, h_cube + off,
+                                      static_cast<size_t>(r1 - r0) * row_px * bands * sizeof(float),
+                                      cudaMemcpyHostToDevice, c.h2d));
+        HSAD_CUDA_TRY(cudaEventRecord(c.ev_h[i], c.h2d));
+        HSAD_CUDA_TRY(cudaStreamWaitEvent(s, c.ev_h[i], 0));
+        if (order > 0) {
+            st = hsad_reduce(static_cast<const float*>(c.cube.p) + off, 4, r1 - r0, samples, bands,
+                             order, target_bands,
+                             static_cast<double*>(c.reduced.p) + static_cast<size_t>(r0) * row_px * target_bands,
+                             8, s);
+            if (st != HSAD_OK) break;
+        }
+        // output rows whose windows lie inside rows [0, r1)
+        int64_t d1 = r1 == lines ? lines : (r1 - rmax) / quantum * quantum;
+        if (d1 <= d_done) continue;
+        hsad_detect_request part[kMaxRequests];
+        for (int q = 0; q < n_requests; ++q) {
+            part[q] = dev_req[q];
+            const int sb = dev_req[q].score_bytes;
+            part[q].d_scores = static_cast<char*>(dev_req[q].d_scores) + d_done * row_px * sb;
+            if (part[q].d_eigcount) part[q].d_eigcount += d_done * row_px;
+        }
+        st = detect_multi_impl(d_det, det_elem, lines, samples, det_bands, 0, r1, d_done, d1, part,
+                               n_requests, d_status, err, s);
+        if (st != HSAD_OK) break;
+        HSAD_CUDA_TRY(cudaEventRecord(c.ev_d[i], s));
+        HSAD_CUDA_TRY(cudaStreamWaitEvent(c.d2h, c.ev_d[i], 0));
+        const size_t rows_px = static_cast<size_t>(d1 - d_done) * row_px;
+        for (int q = 0; q < n_requests; ++q) {
+            const int sb = host_requests[q].score_bytes;
+            HSAD_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(host_requests[q].d_scores) + d_done * row_px * sb,
+                                          part[q].d_scores, rows_px * sb, cudaMemcpyDeviceToHost, c.d2h));
+            if (part[q].d_eigcount)
+                HSAD_CUDA_TRY(cudaMemcpyAsync(host_requests[q].d_eigcount + d_done * row_px,
+                                              part[q].d_eigcount, rows_px, cudaMemcpyDeviceToHost, c.d2h));
+        }
+        d_done = d1;
+    }
+    // drain all three streams before returning (or reporting a launch error)
+    const cudaError_t e1 = cudaStreamSynchronize(c.h2d);
+    const cudaError_t e2 = cudaStreamSynchronize(c.d2h);
+    const cudaError_t e3 = cudaStreamSynchronize(s);
+    if (st != HSAD_OK) return st;
+    HSAD_CUDA_TRY(e1);
+    HSAD_CUDA_TRY(e2);
+    HSAD_CUDA_TRY(e3);
+    unsigned long long packed = 0;
+    HSAD_CUDA_TRY(cudaMemcpy(&packed, d_status, sizeof(packed), cudaMemcpyDeviceToHost));
+    if (packed == ~0ull) return HSAD_OK;
+    // a pixel failed: re-run its row chunk synchronously for the reference message
+    // (identical arithmetic: same rows resident, chunk-aligned range)
+    const int64_t row = static_cast<int64_t>(packed >> 8) / samples;
+    const int64_t a = row / quantum * quantum;
+    const int64_t b = a + quantum < lines ? a + quantum : lines;
+    hsad_detect_request part[kMaxRequests];
+    for (int q = 0; q < n_requests; ++q) {
+        part[q] = dev_req[q];
+        const int sb = dev_req[q].score_bytes;
+        part[q].d_scores = static_cast<char*>(dev_req[q].d_scores) + a * row_px * sb;
+        if (part[q].d_eigcount) part[q].d_eigcount += a * row_px;
+    }
+    st = detect_multi_impl(d_det, det_elem, lines, samples, det_bands, 0, lines, a, b, part,
+                           n_requests, nullptr, err, s);
+    return st != HSAD_OK ? st : set_error(HSAD_E_CUDA, "pipeline: failing pixel not reproduced");
 }

@@ -19,7 +19,6 @@
 //     contiguous 32 x 8 B run.
 // Input fp32 (widened exactly) or fp64; output fp64 or fp32.
 #include <cstdint>
-#include <cstdlib>
 #include <vector>
 
 #include "hsad_internal.h"
@@ -216,136 +215,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
 }
 
-// DMMA variant (TARGET = 4, fp32 cube): Y[8 px x 8] += X[8 px x 4 bands] . Wt[4 x 8]
-// with mma.sync.m8n8k4.f64 (DMMA.8x8x4, the fp64 tensor-core path; columns 4..7 of
-// Wt are zero). One warp instruction performs the 8 x 4 x 4 useful MACs that take 4
-// DFMA instructions per lane in the lane-split kernel, so the DWT costs ~2x fewer
-// issue slots. Fragments (PTX mma.m8n8k4 .f64): lane l holds A[l/4][l%4],
-// B[l%4][l/4], D[l/4][2(l%4) .. 2(l%4)+1].
-// Staging: one bulk copy per pixel into rows of stride L+4 floats (== 4 mod 32 words
-// for L % 32 == 0: the 8 rows of an A fragment hit distinct banks); 3-stage ring.
-template <int BANDS_PAD>
-__global__ void __launch_bounds__(kWarps * 32, 1)
-    reduce_dmma_kernel(const float* __restrict__ cube, int64_t npix, int bands, int tile_px,
-                       int stride, const double* __restrict__ wmap, double* __restrict__ out) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
-    float* stage0 = reinterpret_cast<float*>(smem_raw + 128);
-    const int stage_floats = tile_px * stride;
-    double* s_wt = reinterpret_cast<double*>(stage0 + kStages * stage_floats);  // [BANDS_PAD][4]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < BANDS_PAD * 4; i += kWarps * 32) {
-        const int k = i >> 2, n = i & 3;
-        s_wt[i] = k < bands ? wmap[n * bands + k] : 0.0;
-    }
-    const int64_t full_tiles = npix / tile_px;
-    const uint32_t row_bytes = static_cast<uint32_t>(bands) * 4;
-    const uint32_t tile_bytes = row_bytes * tile_px;
-    // warp 0 issues a tile: lane 0 arms the barrier, every lane copies tile_px/32 rows
-    auto issue = [&](int s, int64_t t) {
-        if (lane == 0) mbar_expect_tx(&bars[s], tile_bytes);
-        __syncwarp();
-        for (int p = lane; p < tile_px; p += 32)
-            bulk_g2s(stage0 + s * stage_floats + p * stride, cube + (t * tile_px + p) * bands,
-                     row_bytes, &bars[s]);
-    };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == 0)
-        for (int s = 0; s < kStages; ++s) {
-            const int64_t t = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
-            if (t < full_tiles) issue(s, t);
-        }
-    const int m = lane >> 2, kq = lane & 3;
-    int64_t it = 0;
-    for (int64_t t = blockIdx.x; t < full_tiles; t += gridDim.x, ++it) {
-        const int s = static_cast<int>(it % kStages);
-        mbar_wait(&bars[s], static_cast<uint32_t>((it / kStages) & 1));
-        const float* tile = stage0 + s * stage_floats;
-        for (int gi = warp; gi < tile_px / 8; gi += kWarps) {
-            const float* arow = tile + (gi * 8 + m) * stride + kq;
-            // four independent accumulator chains (k-steps round-robin) hide DMMA latency
-            double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-            for (int k0 = 0; k0 < bands; k0 += 16) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int kk = k0 + 4 * c;
-                    const double a = kk + kq < bands ? static_cast<double>(arow[kk]) : 0.0;
-                    const double b = (m < 4 && kk < BANDS_PAD) ? s_wt[(kk + kq) * 4 + m] : 0.0;
-                    asm volatile(
-                        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                        : "+d"(d[c][0]), "+d"(d[c][1])
-                        : "d"(a), "d"(b));
-                }
-            }
-            const double d0 = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
-            const double d1 = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
-            if (kq < 2) {
-                const int64_t p = t * tile_px + gi * 8 + m;
-                reinterpret_cast<double2*>(out)[p * 2 + kq] = make_double2(d0, d1);
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const int64_t tn = t + static_cast<int64_t>(kStages) * gridDim.x;
-            if (tn < full_tiles) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(s, tn);
-            }
-        }
-    }
-}
-
-// DMMA reduction, register-direct. For a group of 8 pixels and a block of 16 bands
-// [k0, k0+16), lane l = (m = l/4, q = l%4) loads x[p0+m][k0+4q .. k0+4q+3] with one
-// coalesced float4 (the 8 rows x 64 contiguous bytes of the block) and feeds MMA j
-// (j = 0..3) with A[m][q] = x[m][k0+4q+j]: inside each MMA the K index q stands for
-// band k0+4q+j, the same for every row, so B[q][n] = W[n][k0+4q+j] (from shared
-// memory, padded stride 5 -> conflict-free). Four accumulator chains (one per j).
-// Bands must be a multiple of 16 (the fp32 rows stay 16-byte aligned).
-__global__ void __launch_bounds__(256)
-    reduce_dmma16_kernel(const float* __restrict__ cube, int64_t npix, int bands,
-                         const double* __restrict__ wmap, double* __restrict__ out) {
-    extern __shared__ double s_wt[];  // [bands][5]
-    for (int i = threadIdx.x; i < bands * 4; i += blockDim.x) {
-        const int n = i / bands, k = i % bands;
-        s_wt[k * 5 + n] = wmap[i];
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int m = lane >> 2, q = lane & 3;
-    const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int64_t groups = npix / 8;
-    for (int64_t g = warp; g < groups; g += nwarps) {
-        const float4* row = reinterpret_cast<const float4*>(cube + (g * 8 + m) * bands) + q;
-        double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll 2
-        for (int k0 = 0; k0 < bands; k0 += 16) {
-            const float4 x4 = __ldg(row + (k0 >> 2));
-            const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
-            const double* wrow = s_wt + (k0 + 4 * q) * 5 + m;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double a = static_cast<double>(xs[j]);
-                const double b = m < 4 ? wrow[j * 5] : 0.0;
-                asm volatile(
-                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                    : "+d"(d[j][0]), "+d"(d[j][1])
-                    : "d"(a), "d"(b));
-            }
-        }
-        if (q < 2) {
-            const double d0 = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
-            const double d1 = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
-            reinterpret_cast<double2*>(out)[(g * 8 + m) * 2 + q] = make_double2(d0, d1);
-        }
-    }
-}
-
 // Fallback for targets > 8 or very long spectra: one thread per output value.
 template <typename Tin>
 __global__ void reduce_generic_kernel(const Tin* __restrict__ cube, int64_t npix, int bands,
@@ -403,8 +272,7 @@ cudaError_t launch_tb(const Tin* cube, int64_t npix, int bands, const double* wm
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        int64_t sms = device_sm_count();
-        if (getenv("HSAD_REDUCE_GRID")) sms = atoi(getenv("HSAD_REDUCE_GRID"));  // probe only
+        const int64_t sms = device_sm_count();
         const int grid = static_cast<int>(tiles < sms ? tiles : sms);
         k<<<grid, kWarps * 32, smem, s>>>(cube, npix, bands, tile, wmap, out, out_bytes);
         e = cudaGetLastError();
@@ -447,53 +315,6 @@ cudaError_t launch_reduce(const Tin* cube, int64_t npix, int bands, int target, 
     reduce_generic_kernel<Tin><<<grid_for(npix * target, 256), 256, 0, s>>>(
         cube, npix, bands, target, wmap, out, out_bytes);
     return cudaGetLastError();
-}
-
-// DMMA reduction: fp32 cube, 4 targets, fp64 output, bands a multiple of 4 (per-pixel
-// 16-byte bulk copies). Returns cudaErrorNotSupported for other shapes.
-cudaError_t launch_reduce_dmma(const float* cube, int64_t npix, int bands, const double* wmap,
-                               double* out, cudaStream_t s) {
-    if (bands % 16 == 0 && getenv("HSAD_REDUCE_DMMA16")) {
-        const int64_t groups = npix / 8;
-        int64_t done = 0;
-        if (groups > 0) {
-            const size_t smem = static_cast<size_t>(bands) * 5 * sizeof(double);
-            cudaError_t e = cudaFuncSetAttribute(reduce_dmma16_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            const int grid = device_sm_count() * 8;
-            reduce_dmma16_kernel<<<grid, 256, smem, s>>>(cube, npix, bands, wmap, out);
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return e;
-            done = groups * 8;
-        }
-        if (done < npix) return launch_target<float, 4>(cube + done * bands, npix - done, bands,
-                                                        wmap, out + done * 4, 8, s);
-        return cudaSuccess;
-    }
-    if (bands % 4 != 0 || bands > 256) return cudaErrorNotSupported;
-    const int tile = 64;
-    const int stride = bands + 4;
-    int64_t done = 0;
-    if (npix >= tile) {
-        const int64_t tiles = npix / tile;
-        const size_t smem = 128 + static_cast<size_t>(kStages) * tile * stride * sizeof(float) +
-                            static_cast<size_t>(256) * 4 * sizeof(double);
-        auto k = reduce_dmma_kernel<256>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        const int64_t sms = device_sm_count();
-        const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-        k<<<grid, kWarps * 32, smem, s>>>(cube, npix, bands, tile, stride, wmap, out);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        done = tiles * tile;
-    }
-    if (done < npix) return launch_target<float, 4>(cube + done * bands, npix - done, bands, wmap,
-                                                    out + done * 4, 8, s);
-    return cudaSuccess;
 }
 
 // Per-thread cache of the composed map on the device, keyed by (bands, order, target).
@@ -556,12 +377,6 @@ extern "C" hsad_status hsad_reduce(const void* d_cube, int32_t elem_bytes, int64
     st = device_wavelet_map(bands, order, target_bands, &d_map);
     if (st != HSAD_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (getenv("HSAD_REDUCE_DMMA") && elem_bytes == 4 && target_bands == 4 && out_bytes == 8) {
-        cudaError_t e = launch_reduce_dmma(static_cast<const float*>(d_cube), npix, bands, d_map,
-                                           static_cast<double*>(d_out), s);
-        if (e == cudaSuccess) return HSAD_OK;
-        if (e != cudaErrorNotSupported) return cuda_fail(e, "hsad_reduce dmma launch");
-    }
     cudaError_t e = elem_bytes == 4
                         ? launch_reduce(static_cast<const float*>(d_cube), npix, bands,
                                         target_bands, d_map, d_out, out_bytes, s)

@@ -405,11 +405,11 @@ def test_fullband_dwest_unsupported_and_errors(orc):
     assert str(got.value) == str(want.value)
 
 
-# ------------------------------------------------------------------ fused reduce + detect
+# ------------------------------------------------------------------ reduce + detect in one call
 ALL3 = [("lrx", W1(11), {}), ("dwrx", W2(5, 11), {}), ("dwest", W2(5, 11), {})]
 
 
-def _fused_vs_oracle(orc, cube_np, reqs_spec, order=2, what=""):
+def _rd_vs_oracle(orc, cube_np, reqs_spec, order=2, what=""):
     """hsad_reduce_detect against the oracle's reduce_cube + detectors."""
     cube = gpu(cube_np.astype(np.float32))
     reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in reqs_spec]
@@ -434,12 +434,12 @@ def test_reduce_detect_config_c4(orc):
     cfg = CONFIGS["C4"]
     cube, truth = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"],
                                  cfg["rate"], device=DEV)
-    _, outs = _fused_vs_oracle(orc, host(cube), ALL3, what="C4")
-    # the fused launch and the two-step path agree to DWT rounding
+    _, outs = _rd_vs_oracle(orc, host(cube), ALL3, what="C4")
+    # one call == hsad_reduce then hsad_detect_multi, bit for bit
     reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in ALL3]
     two = hs.detect_multi(hs.reduce_cube(cube, 2, 4), reqs)
     for (a, b), (c, d) in zip(outs, two):
-        assert max_rel_diff(host(a), host(c)) < 1e-9
+        assert torch.equal(a, c)
         if b is not None:
             assert torch.equal(b, d)
 
@@ -452,7 +452,7 @@ def test_reduce_detect_config_c4(orc):
 ])
 def test_reduce_detect_shapes(orc, lines, samples, bands, spec):
     cube = orc.port.random_cube(lines, samples, bands, 4242 + bands)
-    _fused_vs_oracle(orc, cube, spec, what=f"{lines}x{samples}x{bands}")
+    _rd_vs_oracle(orc, cube, spec, what=f"{lines}x{samples}x{bands}")
 
 
 def test_reduce_detect_strip_bit_identical(orc):
@@ -477,13 +477,13 @@ def test_reduce_detect_strip_bit_identical(orc):
 
 
 @pytest.mark.parametrize("bands,target,spec", [
-    (189, 4, ALL3),                              # bands not a multiple of 16: K1 first
-    (64, 8, [("dwrx", W2(3, 7), {})]),           # 8 reduced bands: K1 first
-    (64, 4, [("lrx", W1(25), {})]),              # window reaches past one chunk: K1 first
+    (189, 4, ALL3),
+    (64, 8, [("dwrx", W2(3, 7), {})]),
+    (64, 4, [("lrx", W1(25), {})]),
     (64, 4, [("lrx", W1(3), {}), ("lrx", W1(3), {"guard": 1}), ("dwrx", W2(5, 9), {}),
-             ("dwrx", W2(3, 7), {})]),           # 4 window sizes: K1 first
+             ("dwrx", W2(3, 7), {})]),
 ])
-def test_reduce_detect_fallback_equals_two_step(orc, bands, target, spec):
+def test_reduce_detect_equals_two_step(orc, bands, target, spec):
     cube = gpu(orc.port.random_cube(60, 70, bands, 5).astype(np.float32))
     reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in spec]
     red, outs = hs.reduce_detect(cube, reqs, 2, target)
@@ -494,19 +494,12 @@ def test_reduce_detect_fallback_equals_two_step(orc, bands, target, spec):
         assert torch.equal(a, c)
 
 
-def test_reduce_detect_env_switch_and_empty(orc, monkeypatch):
+def test_reduce_detect_empty_range(orc):
     cube = gpu(orc.port.random_cube(50, 60, 64, 6).astype(np.float32))
     reqs = [hs.DetectRequest("dwest", W2(3, 7), eigcount=True)]
-    red_f, fused = hs.reduce_detect(cube, reqs)
-    monkeypatch.setenv("HSAD_NO_FUSE", "1")
-    red_t, two = hs.reduce_detect(cube, reqs)
-    monkeypatch.delenv("HSAD_NO_FUSE")
-    assert torch.equal(red_t, hs.reduce_cube(cube, 2, 4))
-    assert max_rel_diff(host(red_f), host(red_t)) < 1e-14
-    assert max_rel_diff(host(fused[0][0]), host(two[0][0])) < 1e-9
     # nothing to detect: the reduced cube is still produced
     red_e, outs = hs.reduce_detect(cube, reqs, row_begin=10, row_end=10)
-    assert torch.equal(red_e, red_t) and outs[0][0].numel() == 0
+    assert torch.equal(red_e, hs.reduce_cube(cube, 2, 4)) and outs[0][0].numel() == 0
 
 
 def test_reduce_detect_errors(orc):
@@ -530,7 +523,7 @@ def test_reduce_detect_errors(orc):
     assert e.value.name == "ConfigMismatch"
 
 
-def test_pipeline_host_fused_224(orc):
+def test_pipeline_host_224_bands(orc):
     cube = torch.as_tensor(orc.port.random_cube(120, 130, 224, 8).astype(np.float32))
     reqs = [hs.DetectRequest(a, w, eigcount=(a == "dwest"), **kw) for a, w, kw in ALL3]
     outs = [(torch.empty((120, 130), dtype=r.score_dtype).pin_memory(),
@@ -541,3 +534,23 @@ def test_pipeline_host_fused_224(orc):
         assert torch.equal(a, b.cpu())
         if ac is not None:
             assert torch.equal(ac, bc.cpu())
+
+
+@pytest.mark.parametrize("lines", [5, 400])
+def test_pipeline_host_error_matches_device_path(orc, lines):
+    """Errors from a later strip of the streamed pipeline: same pixel and message."""
+    if lines == 5:
+        cube = np.zeros((5, 5, 64), dtype=np.float32)
+        cube[2, 2] = 1.0
+    else:
+        cube = orc.port.random_cube(lines, 40, 64, 12).astype(np.float32)
+        cube[300:320] = 0.0
+    reqs = [hs.DetectRequest("lrx", W1(3)), hs.DetectRequest("dwrx", W2(1, 3))]
+    with pytest.raises(hs.HsadError) as want:
+        hs.reduce_detect(gpu(cube), reqs)
+    outs = [(torch.empty((lines, cube.shape[1]), dtype=torch.float64), None) for _ in reqs]
+    with pytest.raises(hs.HsadError) as got:
+        hs.pipeline_host(torch.as_tensor(cube), 2, 4, reqs, outs)
+    assert (got.value.name, got.value.row, got.value.col) == (want.value.name, want.value.row,
+                                                              want.value.col)
+    assert str(got.value) == str(want.value)
