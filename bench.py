@@ -42,7 +42,11 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
-WINDOWS = {"lrx": 11, "inner": 5, "outer": 11}
+# BASELINE C5: DWT + all three detectors over the outer-window sweep 7, 11, 15, 21
+# (inner 3 -> 7); LRX uses the outer window (guard 1, the reference's centre-only
+# exclusion). (inner, outer) pairs:
+SWEEP = [(3, 7), (5, 11), (5, 15), (7, 21)]
+RMAX = max(o for _, o in SWEEP) // 2
 
 
 def parse():
@@ -121,15 +125,27 @@ class Clocks:
 
 def requests(hs, score_dtype=torch.float64):
     W1, W2 = hs.WindowConfig.single, hs.WindowConfig.dual
-    return [hs.DetectRequest("lrx", W1(WINDOWS["lrx"]), score_dtype=score_dtype),
-            hs.DetectRequest("dwrx", W2(WINDOWS["inner"], WINDOWS["outer"]), score_dtype=score_dtype),
-            hs.DetectRequest("dwest", W2(WINDOWS["inner"], WINDOWS["outer"]), eigcount=True,
-                             score_dtype=score_dtype)]
+    reqs = []
+    for inner, outer in SWEEP:
+        reqs += [hs.DetectRequest("lrx", W1(outer), score_dtype=score_dtype),
+                 hs.DetectRequest("dwrx", W2(inner, outer), score_dtype=score_dtype),
+                 hs.DetectRequest("dwest", W2(inner, outer), eigcount=True, score_dtype=score_dtype)]
+    return reqs
 
 
 def bytes_per_pixel(bands: int) -> int:
-    # algorithmic: read the fp32 spectrum once, write three fp64 maps + int8 eigen-count
-    return 4 * bands + 3 * 8 + 1
+    # algorithmic: read the fp32 spectrum once, write 12 fp64 maps + 4 int8 eigen-counts
+    return 4 * bands + len(SWEEP) * (3 * 8 + 1)
+
+
+def oracle_step(oracle, cube_np, n, cores):
+    """DWT of the rows the windows of output rows [0, n) need + the 12 detector maps."""
+    red = oracle.port.reduce_cube(cube_np[: min(cube_np.shape[0], n + 2 * RMAX + 1)], 2, 4,
+                                  workers=cores)
+    for inner, outer in SWEEP:
+        oracle.port.local_rx(red, outer, 1e-6, workers=cores, rows=(0, n))
+        oracle.port.dwrx(red, inner, outer, 1e-6, workers=cores, rows=(0, n))
+        oracle.port.dwest(red, inner, outer, 0.1, workers=cores, rows=(0, n))
 
 
 def cpu_baseline(cube_rows_np: np.ndarray, lines: int, rows_total: int, budget_s: float):
@@ -141,22 +157,19 @@ def cpu_baseline(cube_rows_np: np.ndarray, lines: int, rows_total: int, budget_s
     # the sample: rows [0, n) of the workload, DWT of the rows the windows need
     def run(n):
         t0 = time.perf_counter()
-        need = min(L, n + WINDOWS["outer"])
-        red = oracle.port.reduce_cube(cube_rows_np[:need], 2, 4, workers=cores)
-        oracle.port.local_rx(red, WINDOWS["lrx"], 1e-6, workers=cores, rows=(0, n))
-        oracle.port.dwrx(red, WINDOWS["inner"], WINDOWS["outer"], 1e-6, workers=cores, rows=(0, n))
-        oracle.port.dwest(red, WINDOWS["inner"], WINDOWS["outer"], 0.1, workers=cores, rows=(0, n))
+        oracle_step(oracle, cube_rows_np, n, cores)
         return time.perf_counter() - t0
     n, dt = 8, 0.0
     for _ in range(3):  # grow the sample until it takes ~budget_s (or uses every row)
         dt = run(n)
-        if dt >= 0.6 * budget_s or n >= L - WINDOWS["outer"]:
+        if dt >= 0.6 * budget_s or n >= L - 2 * RMAX - 1:
             break
-        n = int(max(8, min(L - WINDOWS["outer"], n * budget_s / max(dt, 1e-3))))
+        n = int(max(8, min(L - 2 * RMAX - 1, n * budget_s / max(dt, 1e-3))))
     px = n * cube_rows_np.shape[1]
     return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "port",
-            "sample": f"rows 0..{n} of the workload ({px} px; DWT on {min(L, n + WINDOWS['outer'])} rows "
-                      f"+ LRX/DWRX/DWEST), {dt:.1f} s, oracle/hsad_oracle.cpp with {cores} threads"}
+            "sample": f"rows 0..{n} of the workload ({px} px; DWT on {min(L, n + 2 * RMAX + 1)} rows "
+                      f"+ LRX/DWRX/DWEST at 4 window pairs), {dt:.1f} s, oracle/hsad_oracle.cpp "
+                      f"with {cores} threads"}
 
 
 def run_reference(args, cfg, rank, world):
@@ -164,18 +177,15 @@ def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
     from harness.scene import generate_rows
-    sample_rows = 48
+    sample_rows = 16
     cube = generate_rows(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], 0,
-                         sample_rows + WINDOWS["outer"], cfg["rate"], device="cpu").numpy()
+                         sample_rows + 2 * RMAX + 1, cfg["rate"], device="cpu").numpy()
     import oracle
     cores = os.cpu_count() or 1
     n = sample_rows
 
     def step():
-        red = oracle.port.reduce_cube(cube, 2, 4, workers=cores)
-        oracle.port.local_rx(red, WINDOWS["lrx"], 1e-6, workers=cores, rows=(0, n))
-        oracle.port.dwrx(red, WINDOWS["inner"], WINDOWS["outer"], 1e-6, workers=cores, rows=(0, n))
-        oracle.port.dwest(red, WINDOWS["inner"], WINDOWS["outer"], 0.1, workers=cores, rows=(0, n))
+        oracle_step(oracle, cube, n, cores)
 
     for _ in range(args.warmup):
         step()
@@ -192,17 +202,21 @@ def run_reference(args, cfg, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, cfg),
         "cpu_baseline": {"value": v, "unit": "Mpixel/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} rows x {cfg['samples']} cols per step (DWT + 3 detectors) of the "
-                                   "workload; CPU restatement (the reference needs Eigen3, absent)"},
+                         "sample": f"{n} rows x {cfg['samples']} cols per step (DWT + 3 detectors x 4 "
+                                   "window pairs) of the workload; CPU restatement (the reference "
+                                   "needs Eigen3, absent)"},
         "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def workload_config(args, cfg):
+    sweep = ", ".join(f"{i}/{o}" for i, o in SWEEP)
     return {"workload": f"{args.config}: {cfg['lines']}x{cfg['samples']}x{cfg['bands']} fp32 BIP, "
-                        f"db4 DWT->4 bands + LRX {WINDOWS['lrx']} + DWRX/DWEST "
-                        f"{WINDOWS['inner']}/{WINDOWS['outer']} (+eigen-count), fp64 maps",
+                        f"db4 DWT->4 bands + LRX/DWRX/DWEST (+DWEST eigen-count) at each "
+                        f"inner/outer window of the sweep {sweep} (LRX on the outer window): "
+                        f"12 fp64 maps per step",
+            "window_sweep": [{"inner": i, "outer": o} for i, o in SWEEP],
             "lines": cfg["lines"], "samples": cfg["samples"], "bands": cfg["bands"],
             "seed": cfg["seed"], "anomaly_rate": cfg["rate"],
             "l2": "inputs larger than L2 (15 GB cube vs 126 MB L2)" if args.config == "C5"
@@ -363,12 +377,11 @@ def run_b200(args, cfg, rank, world, local, dist):
     step_gbs = value * 1e6 * bpp / 1e9
     # DRAM traffic per launch from the committed ncu --set full capture of this workload
     traffic, traffic_src = None, None
-    tfile = ROOT / "profiles" / "ncu_traffic_r1.json"
+    tfile = ROOT / "profiles" / "ncu_traffic_r1_sweep.json"
     if args.config == "C5" and world == 1 and tfile.exists():
         tj = json.loads(tfile.read_text())
-        traffic = sum(tj[k]["dram_read_bytes"] + tj[k]["dram_write_bytes"]
-                      for k in ("reduce_bulk_kernel", "detect_kernel")) / 1e9
-        traffic_src = f"GB per step (reduce + detect launches), {tj['source']}"
+        traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in tj["launches"]) / 1e9
+        traffic_src = f"GB per step (reduce + 4 detect launches), {tj['source']}"
     line = {
         "metric": "Mpixels/sec for DWT+LRX/DWRX/DWEST scoring",
         "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
@@ -380,19 +393,19 @@ def run_b200(args, cfg, rank, world, local, dist):
             "bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
             "frac": step_gbs / peak, "traffic": traffic, "traffic_unit": traffic_src,
             "algorithmic_gb_per_step": bpp * total_px / 1e9 / world,
-            "basis": f"whole step, algorithmic {bpp} B/px (4L fp32 read + 3 fp64 maps + int8 "
-                     f"count) x px/s, {peak_src}",
+            "basis": f"whole step, algorithmic {bpp} B/px (4L fp32 read + 12 fp64 maps + 4 int8 "
+                     f"counts) x px/s, {peak_src}",
             "kernels": {
                 "reduce (K1, HBM-bound)": {"ms": red_ms, "achieved_gbs": red_gbs,
                                            "frac": red_gbs / peak,
                                            "bytes": "fp32 cube read + fp64 reduced write"},
-                "detect (K2-K4 fused, fp64-compute-bound)": {"ms": det_ms,
+                "detect (K2-K4 fused, 4 launches, fp64-compute-bound)": {"ms": det_ms,
                                                              "share": det_ms / (red_ms + det_ms),
                                                              "px_per_s": local_px / (det_ms / 1e3)},
             },
         },
         "clocks": clk,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 + len(SWEEP)) * args.steps,
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline and host_cube is not None:

@@ -1007,12 +1007,16 @@ int64_t row_quantum(int64_t lines, int64_t samples) {
     const int sms = 148;
     const int64_t tw = 128 * kcols_for(samples);
     const int64_t strips = (samples + tw - 1) / tw;
-    int64_t q = 64;
+    // 32 measured best on C5 (24..128 sweep: within 1% of 24, 3.6% faster than 64)
+    int64_t q = 32;
     while (q > 8 && strips * ((lines + q - 1) / q) < 2 * sms) q /= 2;
     return q;
 }
 
-hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
+namespace {
+
+// One fused launch: <= kMaxRequests requests over <= kMaxBoxes window sizes.
+hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
                               int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
                               int64_t row_begin, int64_t row_end,
                               const hsad_detect_request* requests, int32_t n_requests,
@@ -1208,6 +1212,71 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     }
     cudaFreeAsync(status, s);
     return result;
+}
+
+// box radii a request needs (detect.cpp window semantics; LRX guard > 1 adds a box)
+int request_radii(const hsad_detect_request& r, int (&out)[2]) {
+    if (r.window.mode == HSAD_WINDOW_SINGLE) {
+        out[0] = r.window.single_size / 2;
+        if (r.algorithm == HSAD_LRX && r.guard > 1) {
+            out[1] = r.guard / 2;
+            return 2;
+        }
+        return 1;
+    }
+    out[0] = r.window.outer_size / 2;
+    out[1] = r.window.inner_size / 2;
+    return 2;
+}
+
+}  // namespace
+
+// Requests are split greedily, in order, into groups of consecutive requests with
+// the same outer (LRX: single) window, <= kMaxRequests members and <= kMaxBoxes
+// distinct window sizes; each group is one fused launch. The grouping (and so the
+// launch shape) depends only on the request list, so results are deterministic. Synchronous calls report the first group (in request order) with a
+// failing pixel, i.e. the first of the equivalent sequential hsad::detect calls.
+hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
+                              int64_t row_begin, int64_t row_end,
+                              const hsad_detect_request* requests, int32_t n_requests,
+                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s) {
+    if (n_requests < 1 || n_requests > kMaxCallRequests || !requests)
+        return set_error(HSAD_E_INVALID_VALUE, "between 1 and " + std::to_string(kMaxCallRequests) +
+                                                   " requests per call");
+    int g0 = 0;
+    while (g0 < n_requests) {
+        int radii[kMaxBoxes], nr = 0, g1 = g0;
+        int outer0[2];
+        request_radii(requests[g0], outer0);
+        while (g1 < n_requests && g1 - g0 < kMaxRequests) {
+            int rq[2];
+            const int k = request_radii(requests[g1], rq);
+            // a group shares one outer window (the fused kernel's standard layout)
+            if (g1 > g0 && rq[0] != outer0[0]) break;
+            int add = 0, merged[kMaxBoxes + 2];
+            for (int i = 0; i < nr; ++i) merged[i] = radii[i];
+            for (int j = 0; j < k; ++j) {
+                bool seen = false;
+                for (int i = 0; i < nr + add; ++i) seen = seen || merged[i] == rq[j];
+                if (!seen) merged[nr + add++] = rq[j];
+            }
+            if (nr + add > kMaxBoxes && g1 > g0) break;
+            if (nr + add > kMaxBoxes) {  // a single request never needs more than 2
+                ++g1;
+                break;
+            }
+            for (int i = nr; i < nr + add; ++i) radii[i] = merged[i];
+            nr += add;
+            ++g1;
+        }
+        hsad_status st = detect_group_impl(d_cube, elem_bytes, lines, samples, bands, buf_row0,
+                                           buf_rows, row_begin, row_end, requests + g0, g1 - g0,
+                                           d_status, err, s);
+        if (st != HSAD_OK) return st;
+        g0 = g1;
+    }
+    return HSAD_OK;
 }
 
 }  // namespace hsad_b200

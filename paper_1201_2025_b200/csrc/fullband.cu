@@ -16,9 +16,26 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "hsad_internal.h"
+
+#ifdef HSAD_PHASE_TIMERS
+__device__ unsigned long long g_fb_cycles[8];
+#define FB_MARK(i)                                                              \
+    do {                                                                        \
+        if (threadIdx.x == 0) {                                                 \
+            const long long fb_t1 = clock64();                                  \
+            atomicAdd(&g_fb_cycles[i], (unsigned long long)(fb_t1 - fb_t0));    \
+            fb_t0 = fb_t1;                                                      \
+        }                                                                       \
+    } while (0)
+#else
+#define FB_MARK(i) \
+    do {           \
+    } while (0)
+#endif
 
 namespace hsad_b200 {
 
@@ -75,6 +92,16 @@ __device__ __forceinline__ int64_t sample_base(const FbParams& P, int r, int c, 
     return (static_cast<int64_t>(rr) * P.samples + cc) * P.bands;
 }
 
+// fp64 reciprocal of a positive finite pivot: MUFU seed + two Newton steps (~1 ulp)
+__device__ __forceinline__ double fb_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
 __device__ __forceinline__ int packed(int i, int k) { return i * (i + 1) / 2 + k; }  // k <= i
 
 __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams P) {
@@ -91,6 +118,9 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
     const int c = blockIdx.x;
     const int64_t r = P.row_begin + blockIdx.y;
     if (r >= P.row_end) return;
+#ifdef HSAD_PHASE_TIMERS
+    long long fb_t0 = clock64();
+#endif
     const int ri = static_cast<int>(r);
     // sample sets: LRX background = window minus the guard box (centre when guard 1);
     // DWRX covariance = annulus (outer minus inner box), d = mean(inner) - mean(annulus)
@@ -115,6 +145,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
         mu[MP + b] = (b < L && P.algo == HSAD_DWRX) ? si / (excl * excl) : 0.0;
     }
     __syncthreads();
+    FB_MARK(0);
 
     // pass 2: centred Gram, 4x4 tiles of the lower triangle, in groups of
     // kFbThreads * kFbMaxTiles tiles (one group for L <= 196, two for L = 224)
@@ -177,6 +208,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
         }
     }
     __syncthreads();
+    FB_MARK(1);
     // displacement d and ridge; border row L holds d, (L, L) = 0; rows > L are inert
     if (t == 0) {
         double tr = 0.0;
@@ -211,44 +243,50 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
     const int64_t lin = r * P.samples + c;
     if (lin == P.diag_lin && t == 0) *P.diag_out = delta;
     double score = 0.0;
+    FB_MARK(2);
     if (any_d) {
         // Blocked right-looking Cholesky of the bordered matrix (rows 0..L; the border
         // row L is updated like any row and its diagonal ends as the Schur complement).
-        // Per 8-column panel: warp 0 factors the panel warp-synchronously, then every
-        // thread applies the rank-8 update to 4x4 tiles of the trailing lower triangle.
+        // Column j of the factor is kept UNSCALED in A (l_ij = A[i][j] * rinv[j]), so a
+        // panel step never writes the column it reads: per column one barrier, every
+        // thread one row of the panel update. Then every thread applies the rank-PB
+        // update to 4x4 tiles of the trailing lower triangle.
         constexpr int PB = 8;
-        const int warp = t >> 5, lane = t & 31;
+        double* rinv = col;  // [MP] 1 / sqrt(pivot) per factored column
         for (int j0 = 0; j0 < L; j0 += PB) {
             const int jend = min(j0 + PB, L);  // panel columns [j0, jend)
-            if (warp == 0) {
-                for (int jj = j0; jj < jend; ++jj) {
-                    const double p = A[packed(jj, jj)];
-                    if (lane == 0) {
-                        if (!(p > 0.0)) s_bad = 1;
-                        s_dmax = fmax(s_dmax, fabs(p));
-                        s_dmin = fmin(s_dmin, p);
-                    }
-                    if (!(p > 0.0)) break;  // warp-uniform (every lane read the same p)
-                    const double rinv = rsqrt(p);
-                    for (int i = jj + 1 + lane; i <= L; i += 32) A[packed(i, jj)] *= rinv;
-                    __syncwarp();
-                    // update the rest of the panel: rows i > jj, columns jj < k < jend, k <= i
-                    for (int i = jj + 1 + lane; i <= L; i += 32) {
-                        const double lij = A[packed(i, jj)];
-                        const int kmax = min(i, jend - 1);
-                        for (int k = jj + 1; k <= kmax; ++k)
-                            A[packed(i, k)] = fma(-lij, A[packed(k, jj)], A[packed(i, k)]);
-                    }
-                    __syncwarp();
+            for (int jj = j0; jj < jend; ++jj) {
+                const double p = A[packed(jj, jj)];
+                if (!(p > 0.0)) {  // uniform: every thread read the same pivot
+                    if (t == 0) s_bad = 1;
+                    break;
                 }
+                const double ri = rsqrt(p);
+                if (t == 0) {
+                    s_dmax = fmax(s_dmax, fabs(p));
+                    s_dmin = fmin(s_dmin, p);
+                    rinv[jj] = ri;
+                }
+                // rows i > jj, columns jj < k < jend, k <= i
+                for (int i = jj + 1 + t; i <= L; i += kFbThreads) {
+                    const double lij = A[packed(i, jj)] * ri;
+                    const int kmax = min(i, jend - 1);
+                    for (int k = jj + 1; k <= kmax; ++k)
+                        A[packed(i, k)] = fma(-lij, A[packed(k, jj)] * ri, A[packed(i, k)]);
+                }
+                __syncthreads();
             }
             __syncthreads();
+            FB_MARK(4);
             if (s_bad) break;
             // trailing update: rows i in [jend, L], columns k in [jend, i]
             const int n = L + 1 - jend;            // trailing rows
             const int nb = (n + 3) / 4;            // 4-row blocks
             const int nblocks = nb * (nb + 1) / 2;
             const int w = jend - j0;               // panel width
+            double rp[PB];
+#pragma unroll
+            for (int q = 0; q < PB; ++q) rp[q] = q < w ? rinv[j0 + q] : 0.0;
             for (int blk = t; blk < nblocks; blk += kFbThreads) {
                 int bi = static_cast<int>((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
                 while ((bi + 1) * (bi + 2) / 2 <= blk) ++bi;
@@ -260,8 +298,8 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
                     for (int q = 0; q < PB; ++q) {
-                        li[a][q] = (i0 + a <= L && q < w) ? A[packed(i0 + a, j0 + q)] : 0.0;
-                        lk[a][q] = (k0 + a <= L && q < w) ? A[packed(k0 + a, j0 + q)] : 0.0;
+                        li[a][q] = (i0 + a <= L && q < w) ? A[packed(i0 + a, j0 + q)] * rp[q] : 0.0;
+                        lk[a][q] = (k0 + a <= L && q < w) ? A[packed(k0 + a, j0 + q)] * rp[q] : 0.0;
                     }
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
@@ -279,9 +317,11 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
                 }
             }
             __syncthreads();
+            FB_MARK(5);
         }
         if (t == 0) s_piv = A[packed(L, L)];
         __syncthreads();
+        FB_MARK(3);
         if (t == 0) {
             const bool singular = s_bad || !(s_dmax > 0.0) || s_dmin <= s_dmax * 1e-14;
             if (singular) {
@@ -305,17 +345,266 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
     }
 }
 
+// ---- register-resident variant (bands + 1 <= 192) ----------------------------
+// Same arithmetic contract as fullband_kernel, but the bordered matrix never goes
+// to shared memory: thread t owns one 8x8 tile (ti, tk), ti >= tk, of the lower
+// triangle. The centred Gram accumulates into that tile (64 fp64 accumulators,
+// 16 doubles of shared-memory reads per 64 FMAs), and the right-looking Cholesky
+// then runs on the same registers: per column j the owners of tile column j/8
+// publish the (unscaled) column c to shared memory (double-buffered, one barrier
+// per column), and every live tile applies a_ik -= c_i (c_k / c_j). The pivots
+// c_j are the LDLT D_j of the singular rule; the last Schur pivot is -score.
+constexpr int kFbRegMaxMp = 192;  // 24 tile rows -> 300 tiles -> <= 320 threads
+constexpr int kFbRegThreads = 320;
+
+__global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const FbParams P) {
+    extern __shared__ double sm[];
+    const int L = P.bands, MP = P.mp, CH = P.chunk;
+    // 8-band blocks are padded so that lanes reading different blocks hit different
+    // banks: xs blocks of 10 doubles (16-byte aligned), published columns of 9
+    const int S = (MP / 8) * 10;                       // xs row stride
+    const int CB = (MP / 8) * 9;                       // published column length
+    double* xs = sm;                                   // [CH][S] centred samples
+    double* mu = xs + static_cast<int64_t>(CH) * S;    // [2][MP] means (window / inner box)
+    double* cb = mu + 2 * MP;                          // [2][CB] published Cholesky columns
+    double* dg = cb + 2 * CB;                          // [MP] diagonal of C / displacement d
+    __shared__ double s_piv, s_dmax, s_dmin;
+    __shared__ int s_bad;
+
+    const int t = threadIdx.x;
+    const int c = blockIdx.x;
+    const int64_t r = P.row_begin + blockIdx.y;
+    if (r >= P.row_end) return;
+    const int ri = static_cast<int>(r);
+#ifdef HSAD_PHASE_TIMERS
+    long long fb_t0 = clock64();
+#endif
+    const int size = P.outer, excl = P.inner;
+    const int N = size * size - excl * excl;
+    int64_t* base = reinterpret_cast<int64_t*>(dg + MP);  // [N + excl^2]
+    const int NI = P.algo == HSAD_DWRX ? excl * excl : 0;
+    for (int k = t; k < N + NI; k += blockDim.x)
+        base[k] = k < N ? sample_base(P, ri, c, k, size, excl) : sample_base(P, ri, c, k - N, excl, 0);
+    __syncthreads();
+    for (int b = t; b < MP; b += blockDim.x) {
+        double sum = 0.0, si = 0.0;
+        if (b < L) {
+            for (int k = 0; k < N; ++k) sum += ld(P, base[k] + b);
+            for (int k = 0; k < NI; ++k) si += ld(P, base[N + k] + b);
+        }
+        mu[b] = b < L ? sum / N : 0.0;
+        mu[MP + b] = (b < L && P.algo == HSAD_DWRX) ? si / (excl * excl) : 0.0;
+    }
+    __syncthreads();
+    FB_MARK(0);
+
+    // this thread's tile of the lower triangle
+    const int T = MP / 8;
+    const int ntiles = T * (T + 1) / 2;
+    const bool own = t < ntiles;
+    int ti = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    const int tk = own ? t - ti * (ti + 1) / 2 : 0;
+    if (!own) ti = 0;
+    double acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < N; k0 += CH) {
+        const int nk = min(CH, N - k0);
+        __syncthreads();
+        for (int e = t; e < nk * MP; e += blockDim.x) {
+            const int k = e / MP, b = e % MP;
+            xs[k * S + (b >> 3) * 10 + (b & 7)] = b < L ? ld(P, base[k0 + k] + b) - mu[b] : 0.0;
+        }
+        __syncthreads();
+        if (own) {
+            const double* xa = xs + 10 * ti;
+            const double* xb = xs + 10 * tk;
+            for (int k = 0; k < nk; ++k) {
+                double av[8], bv[8];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double2 a2 = *reinterpret_cast<const double2*>(xa + k * S + 2 * h);
+                    const double2 b2 = *reinterpret_cast<const double2*>(xb + k * S + 2 * h);
+                    av[2 * h] = a2.x;
+                    av[2 * h + 1] = a2.y;
+                    bv[2 * h] = b2.x;
+                    bv[2 * h + 1] = b2.y;
+                }
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            }
+        }
+    }
+    // covariance (divisor N); diagonal to shared memory for the trace
+    const double invN = 1.0 / N;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] *= invN;
+    if (own && ti == tk)
+#pragma unroll
+        for (int a = 0; a < 8; ++a) dg[8 * ti + a] = acc[a][a];
+    __syncthreads();
+    FB_MARK(1);
+    if (t == 0) {
+        double tr = 0.0;
+        for (int b = 0; b < L; ++b) tr += dg[b];
+        s_piv = P.ridge * tr / L;  // delta
+        s_bad = 0;
+        s_dmax = 0.0;
+        s_dmin = DBL_MAX;
+    }
+    __syncthreads();
+    const double delta = s_piv;
+    // displacement d (border row L), ridge on the diagonal
+    double dmaxabs = 0.0;
+    for (int b = t; b < L; b += blockDim.x) {
+        double d;
+        if (P.algo == HSAD_LRX) {
+            const int rr = mirror_fb(ri, static_cast<int>(P.lines)) - static_cast<int>(P.buf_row0);
+            d = ld(P, (static_cast<int64_t>(rr) * P.samples + c) * L + b) - mu[b];
+        } else {
+            d = mu[MP + b] - mu[b];
+        }
+        dg[b] = d;
+        dmaxabs = fmax(dmaxabs, fabs(d));
+    }
+    const int any_d = __syncthreads_or(dmaxabs > 0.0);
+    if (own) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int i = 8 * ti + a;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int k = 8 * tk + b;
+                if (i == k && i < L) acc[a][b] += delta;
+                if (i == L) acc[a][b] = k < L ? dg[k] : 0.0;  // border row; corner 0
+            }
+        }
+    }
+    const int64_t o = (r - P.row_begin) * P.samples + c;
+    const int64_t lin = r * P.samples + c;
+    if (lin == P.diag_lin && t == 0) *P.diag_out = delta;
+    FB_MARK(2);
+    double score = 0.0;
+    if (any_d) {
+        // columns j = 8 jt + jc; jc is unrolled so the published column is a static
+        // register index (a runtime index would push the tile to local memory)
+        bool stop = false;
+        for (int jt = 0; jt * 8 < L && !stop; ++jt) {
+#pragma unroll
+            for (int jc = 0; jc < 8; ++jc) {
+                const int j = 8 * jt + jc;
+                if (j >= L || stop) break;  // uniform
+                double* col = cb + (j & 1) * CB;  // row i at 9 (i / 8) + i % 8
+                if (own && tk == jt)
+#pragma unroll
+                    for (int a = 0; a < 8; ++a)
+                        if (8 * ti + a >= j) col[9 * ti + a] = acc[a][jc];
+                __syncthreads();
+                const double p = col[9 * jt + jc];
+                if (!(p > 0.0)) {  // uniform: every thread read the same pivot
+                    if (t == 0) s_bad = 1;
+                    stop = true;
+                    break;
+                }
+                if (t == 0) {
+                    s_dmax = fmax(s_dmax, fabs(p));
+                    s_dmin = fmin(s_dmin, p);
+                }
+                if (own && (tk > jt || (tk == jt && jc < 7))) {
+                    const double pinv = fb_rcp(p);
+                    double ci[8], ck[8];
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {
+                        ci[a] = col[9 * ti + a];
+                        ck[a] = col[9 * tk + a] * pinv;
+                    }
+#pragma unroll
+                    for (int a = 0; a < 8; ++a)
+#pragma unroll
+                        for (int b = 0; b < 8; ++b)
+                            if (tk > jt || b > jc) acc[a][b] = fma(-ci[a], ck[b], acc[a][b]);
+                }
+            }
+        }
+        // Schur complement of the border corner
+        if (own && ti == (L >> 3) && tk == ti)
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    if (8 * ti + a == L && 8 * tk + b == L) s_piv = acc[a][b];
+        __syncthreads();
+        FB_MARK(3);
+        if (t == 0) {
+            const bool singular = s_bad || !(s_dmax > 0.0) || s_dmin <= s_dmax * 1e-14;
+            if (singular) {
+                atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
+                                        HSAD_E_SINGULAR_AFTER_RIDGE);
+            } else {
+                score = -s_piv;
+                if (!isfinite(score)) {
+                    atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
+                                            (HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
+                    score = 0.0;
+                }
+            }
+        }
+    }
+    if (t == 0) {
+        score = P.algo == HSAD_LRX ? fmax(score, 0.0) : fabs(score);
+        if (P.score_bytes == 8) static_cast<double*>(P.scores)[o] = score;
+        else static_cast<float*>(P.scores)[o] = static_cast<float>(score);
+    }
+}
+
 }  // namespace
+
+#ifdef HSAD_PHASE_TIMERS
+extern "C" void hsad_fb_phase_cycles(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_fb_cycles, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_fb_cycles, z, sizeof(z));
+    }
+}
+#endif
 
 // Shared memory and launch shape for one full-band request.
 hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
     if (P.bands > kFbMaxBands)
         return set_error(HSAD_E_UNSUPPORTED, "full-band detection supports at most " +
                                                  std::to_string(kFbMaxBands) + " bands");
+    const int64_t rows = P.row_end - P.row_begin;
+    if (rows > 65535) return set_error(HSAD_E_UNSUPPORTED, "strip too tall for one launch");
+    dim3 grid(static_cast<unsigned>(P.samples), static_cast<unsigned>(rows));
+    const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;  // >= N + inner^2
+    const int mp8 = ((P.bands + 1) + 7) / 8 * 8;
+    if (mp8 <= kFbRegMaxMp && !getenv("HSAD_FB_PACKED")) {
+        // register-resident tiles: shared memory holds only samples and vectors
+        P.mp = mp8;
+        P.chunk = 32;
+        const size_t smem =
+            (static_cast<size_t>(P.chunk) * (P.mp / 8) * 10 + 3 * P.mp + 2 * (P.mp / 8) * 9 + nsamp) * 8;
+        HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_reg_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+        const int T = P.mp / 8;
+        const int nt = (T * (T + 1) / 2 + 31) / 32 * 32;
+        fullband_reg_kernel<<<grid, nt, smem, s>>>(P);
+        HSAD_CUDA_TRY(cudaGetLastError());
+        return HSAD_OK;
+    }
     P.mp = ((P.bands + 1) + 3) / 4 * 4;
     const int64_t tri = static_cast<int64_t>(P.mp) * (P.mp + 1) / 2;
     int chunk = 32;
-    const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;  // >= N + inner^2
     auto bytes = [&](int ch) {
         return (tri + static_cast<int64_t>(ch) * P.mp + 3 * P.mp + nsamp) * 8;
     };
@@ -326,9 +615,6 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(bytes(chunk));
     HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
-    const int64_t rows = P.row_end - P.row_begin;
-    if (rows > 65535) return set_error(HSAD_E_UNSUPPORTED, "strip too tall for one launch");
-    dim3 grid(static_cast<unsigned>(P.samples), static_cast<unsigned>(rows));
     fullband_kernel<<<grid, kFbThreads, smem, s>>>(P);
     HSAD_CUDA_TRY(cudaGetLastError());
     return HSAD_OK;

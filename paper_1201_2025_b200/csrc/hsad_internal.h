@@ -64,7 +64,8 @@ struct FbParams {
 // Kernel-side limits.
 constexpr int kMaxDetectBands = 8;
 constexpr int kMaxBoxes = 4;
-constexpr int kMaxRequests = 4;
+constexpr int kMaxRequests = 4;       // per fused detector launch
+constexpr int kMaxCallRequests = 16;  // per hsad_detect_multi / hsad_pipeline_host call
 constexpr int kMaxRadius = 112;  // window edge <= 225 (block of 256 columns)
 constexpr int kMaxReduceBands = 4096;
 

@@ -58,7 +58,7 @@ struct DevBuf {
 constexpr int kMaxStrips = 16;
 
 struct PipelineCache {
-    DevBuf cube, reduced, out[kMaxRequests], counts[kMaxRequests], status;
+    DevBuf cube, reduced, out[kMaxCallRequests], counts[kMaxCallRequests], status;
     int device = -1;
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_h[kMaxStrips] = {}, ev_d[kMaxStrips] = {}, ev_start = nullptr;
@@ -103,8 +103,8 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
     }
     if (lines < 0 || samples < 0) return set_error(HSAD_E_INVALID_VALUE, "negative cube extent");
     if (!h_cube && lines * samples * bands > 0) return set_error(HSAD_E_INVALID_VALUE, "null cube");
-    if (n_requests < 1 || n_requests > kMaxRequests || !host_requests)
-        return set_error(HSAD_E_INVALID_VALUE, "between 1 and 4 requests per call");
+    if (n_requests < 1 || n_requests > kMaxCallRequests || !host_requests)
+        return set_error(HSAD_E_INVALID_VALUE, "between 1 and 16 requests per call");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t npix = lines * samples;
     const int32_t det_bands = order > 0 ? target_bands : bands;
@@ -124,7 +124,7 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
         d_det = c.reduced.p;
         det_elem = 8;
     }
-    hsad_detect_request dev_req[kMaxRequests];
+    hsad_detect_request dev_req[kMaxCallRequests];
     for (int q = 0; q < n_requests; ++q) {
         dev_req[q] = host_requests[q];
         const int sb = host_requests[q].score_bytes;
@@ -180,7 +180,7 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
         // output rows whose windows lie inside rows [0, r1)
         int64_t d1 = r1 == lines ? lines : (r1 - rmax) / quantum * quantum;
         if (d1 <= d_done) continue;
-        hsad_detect_request part[kMaxRequests];
+        hsad_detect_request part[kMaxCallRequests];
         for (int q = 0; q < n_requests; ++q) {
             part[q] = dev_req[q];
             const int sb = dev_req[q].score_bytes;
@@ -219,7 +219,7 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
     const int64_t row = static_cast<int64_t>(packed >> 8) / samples;
     const int64_t a = row / quantum * quantum;
     const int64_t b = a + quantum < lines ? a + quantum : lines;
-    hsad_detect_request part[kMaxRequests];
+    hsad_detect_request part[kMaxCallRequests];
     for (int q = 0; q < n_requests; ++q) {
         part[q] = dev_req[q];
         const int sb = dev_req[q].score_bytes;

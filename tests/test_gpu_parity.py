@@ -554,3 +554,60 @@ def test_pipeline_host_error_matches_device_path(orc, lines):
     assert (got.value.name, got.value.row, got.value.col) == (want.value.name, want.value.row,
                                                               want.value.col)
     assert str(got.value) == str(want.value)
+
+
+# ------------------------------------------------------------------ request groups (C5 sweep)
+SWEEP = [(3, 7), (5, 11), (5, 15), (7, 21)]
+
+
+def _sweep_requests():
+    reqs = []
+    for i, o in SWEEP:
+        reqs += [hs.DetectRequest("lrx", W1(o)), hs.DetectRequest("dwrx", W2(i, o)),
+                 hs.DetectRequest("dwest", W2(i, o), eigcount=True)]
+    return reqs
+
+
+def test_sweep_in_one_call_equals_per_pair_calls(orc):
+    red = orc.port.random_cube(90, 140, 4, 31)
+    cube = gpu(red)
+    reqs = _sweep_requests()
+    allq = hs.detect_multi(cube, reqs)  # 12 requests -> 4 fused launches
+    for g in range(4):
+        part = hs.detect_multi(cube, reqs[3 * g:3 * g + 3])
+        for (a, b), (c, d) in zip(allq[3 * g:3 * g + 3], part):
+            assert torch.equal(a, c)
+            if b is not None:
+                assert torch.equal(b, d)
+    i, o = SWEEP[3]
+    assert max_rel_diff(host(allq[9][0]), orc.port.local_rx(red, o, 1e-6, workers=8)) < TOL64
+    want, wc = orc.port.dwest(red, i, o, 0.1, workers=8)
+    assert max_rel_diff(host(allq[11][0]), want) < TOL64
+    assert np.array_equal(host(allq[11][1]), wc)
+    # requests with different outer windows run as separate launches (LRX 3 .. 11)
+    many = [hs.DetectRequest("lrx", W1(w)) for w in (3, 5, 7, 9, 11)]
+    got = hs.detect_multi(cube, many)
+    for r, (s, _) in zip(many, got):
+        assert torch.equal(s, hs.detect_multi(cube, [r])[0][0])
+    # one outer window with more than 4 requests / window sizes: split, same values
+    # up to the launch shape's rounding
+    mixed = [hs.DetectRequest("dwrx", W2(i, 15)) for i in (1, 3, 5, 7, 9)]
+    got = hs.detect_multi(cube, mixed)
+    for (i, r), (s, _) in zip(zip((1, 3, 5, 7, 9), mixed), got):
+        assert max_rel_diff(host(s), orc.port.dwrx(red, i, 15, 1e-6, workers=8)) < TOL64
+    with pytest.raises(hs.HsadError) as e:
+        hs.detect_multi(cube, [hs.DetectRequest("lrx", W1(3))] * 17)
+    assert e.value.name == "InvalidValue"
+
+
+def test_pipeline_host_sweep_equals_device_path(orc):
+    cube = torch.as_tensor(orc.port.random_cube(150, 90, 64, 17).astype(np.float32))
+    reqs = _sweep_requests()
+    outs = [(torch.empty((150, 90), dtype=r.score_dtype).pin_memory(),
+             torch.empty((150, 90), dtype=torch.int8) if r.eigcount else None) for r in reqs]
+    hs.pipeline_host(cube.pin_memory(), 2, 4, reqs, outs)
+    dev = hs.detect_multi(hs.reduce_cube(cube.to(DEV), 2, 4), reqs)
+    for (a, ac), (b, bc) in zip(outs, dev):
+        assert torch.equal(a, b.cpu())
+        if ac is not None:
+            assert torch.equal(ac, bc.cpu())
