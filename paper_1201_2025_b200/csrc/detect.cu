@@ -444,9 +444,15 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
         }
     }
     // polish sweeps (warp-uniform) until the off-diagonal mass is below
-    // (1e-15 |B|)^2; larger matrices leave fp32 less converged and need more
+    // (1e-12 |B|)^2: eigenvalues are then exact to ~1e-24 |B| and eigenvectors to
+    // ~1e-12 / relative gap, three orders inside the 1e-9 score gate. After the fp32
+    // stage (off ~1e-7) one quadratic sweep gets there; larger matrices leave fp32
+    // less converged and take more
 #pragma unroll 1
     for (int sweep = 0; sweep < 8; ++sweep) {
+#ifdef HSAD_PHASE_TIMERS
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[7], 1ull);  // warp polish sweeps
+#endif
         sweep64<L>(B, V);
         {
             double off = 0.0, dia = 0.0;
@@ -456,7 +462,7 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
 #pragma unroll
                 for (int j = i + 1; j < L; ++j) off = fma(B[i][j], B[i][j], off);
             }
-            if (__all_sync(__activemask(), off <= 1e-30 * dia)) break;
+            if (__all_sync(__activemask(), off <= 1e-24 * dia)) break;
         }
     }
 #pragma unroll
