@@ -92,14 +92,12 @@ __device__ __forceinline__ int64_t sample_base(const FbParams& P, int r, int c, 
     return (static_cast<int64_t>(rr) * P.samples + cc) * P.bands;
 }
 
-// fp64 reciprocal of a positive finite pivot: MUFU seed + two Newton steps (~1 ulp)
-__device__ __forceinline__ double fb_rcp(double x) {
+__device__ __forceinline__ double fb_rsqrt(double x) {
     double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-x, y, 1.0);
-    return fma(y, e, y);
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
 }
 
 __device__ __forceinline__ int packed(int i, int k) { return i * (i + 1) / 2 + k; }  // k <= i
@@ -363,12 +361,12 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     // 8-band blocks are padded so that lanes reading different blocks hit different
     // banks: xs blocks of 10 doubles (16-byte aligned), published columns of 9
     const int S = (MP / 8) * 10;                       // xs row stride
-    const int CB = (MP / 8) * 9;                       // published column length
+    const int CBP = (MP / 8) * 10;                     // panel column length (padded rows)
     double* xs = sm;                                   // [CH][S] centred samples
     double* mu = xs + static_cast<int64_t>(CH) * S;    // [2][MP] means (window / inner box)
-    double* cb = mu + 2 * MP;                          // [2][CB] published Cholesky columns
-    double* dg = cb + 2 * CB;                          // [MP] diagonal of C / displacement d
-    __shared__ double s_piv, s_dmax, s_dmin;
+    double* lpt = mu + 2 * MP;                         // [2][8 CBP + 8] Cholesky panels
+    double* dg = lpt + 2 * (8 * CBP + 8);              // [MP] diagonal of C / displacement d
+    __shared__ double s_piv, s_dmax, s_dmin, s_corner[8];
     __shared__ int s_bad;
 
     const int t = threadIdx.x;
@@ -415,9 +413,17 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     for (int k0 = 0; k0 < N; k0 += CH) {
         const int nk = min(CH, N - k0);
         __syncthreads();
-        for (int e = t; e < nk * MP; e += blockDim.x) {
-            const int k = e / MP, b = e % MP;
-            xs[k * S + (b >> 3) * 10 + (b & 7)] = b < L ? ld(P, base[k0 + k] + b) - mu[b] : 0.0;
+        // one band per thread, all samples of the chunk (coalesced across the warp,
+        // 8 independent loads in flight per thread, no integer division)
+        for (int b = t; b < MP; b += blockDim.x) {
+            double* dst = xs + (b >> 3) * 10 + (b & 7);
+            if (b < L) {
+                const double m = mu[b];
+#pragma unroll 8
+                for (int k = 0; k < nk; ++k) dst[k * S] = ld(P, base[k0 + k] + b) - m;
+            } else {
+                for (int k = 0; k < nk; ++k) dst[k * S] = 0.0;
+            }
         }
         __syncthreads();
         if (own) {
@@ -494,53 +500,97 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     FB_MARK(2);
     double score = 0.0;
     if (any_d) {
-        // columns j = 8 jt + jc; jc is unrolled so the published column is a static
-        // register index (a runtime index would push the tile to local memory)
-        bool stop = false;
-        for (int jt = 0; jt * 8 < L && !stop; ++jt) {
+        // Blocked right-looking Cholesky on the register tiles, one 8-column tile
+        // column jt per step (2 barriers per step, panel buffer double-buffered):
+        //   1. the owner of diagonal tile (jt, jt) factors it alone (pivots p_j are the
+        //      LDLT D_j of the singular rule) and publishes L_jj and 1/L_jj[c][c];
+        //   2. the owners of tiles (ti > jt, jt) solve X = A L_jj^-T in registers and
+        //      publish X (the panel) column-major;
+        //   3. every tile (ti >= tk > jt) applies acc -= X_ti X_tk^T (512 FMAs; per
+        //      panel column two 8-double vectors, 4 LDS.128 each).
+        // Columns >= L (border, padding) are never factored; the border corner then
+        // holds 0 - d^T (C + delta I)^-1 d = -score.
+        const int LT = L >> 3;  // tile column holding the border row/column
+        for (int jt = 0; jt <= LT; ++jt) {
+            double* lp = lpt + (jt & 1) * (8 * CBP + 8);  // [8][CBP] panel, then [8] 1/diag
+            double* rdiag = lp + 8 * CBP;
+            if (own && ti == jt && tk == jt) {
+                bool bad = false;
+                double dmax = s_dmax, dmin = s_dmin;
 #pragma unroll
-            for (int jc = 0; jc < 8; ++jc) {
-                const int j = 8 * jt + jc;
-                if (j >= L || stop) break;  // uniform
-                double* col = cb + (j & 1) * CB;  // row i at 9 (i / 8) + i % 8
-                if (own && tk == jt)
+                for (int jc = 0; jc < 8; ++jc) {
+                    if (8 * jt + jc < L && !bad) {
+                        const double p = acc[jc][jc];
+                        if (!(p > 0.0)) {
+                            bad = true;
+                        } else {
+                            dmax = fmax(dmax, fabs(p));
+                            dmin = fmin(dmin, p);
+                            const double r = fb_rsqrt(p);
+                            rdiag[jc] = r;
+                            acc[jc][jc] = p * r;
 #pragma unroll
-                    for (int a = 0; a < 8; ++a)
-                        if (8 * ti + a >= j) col[9 * ti + a] = acc[a][jc];
-                __syncthreads();
-                const double p = col[9 * jt + jc];
-                if (!(p > 0.0)) {  // uniform: every thread read the same pivot
-                    if (t == 0) s_bad = 1;
-                    stop = true;
-                    break;
+                            for (int a2 = jc + 1; a2 < 8; ++a2) acc[a2][jc] *= r;
+#pragma unroll
+                            for (int b2 = jc + 1; b2 < 8; ++b2)
+#pragma unroll
+                                for (int a2 = b2; a2 < 8; ++a2)
+                                    acc[a2][b2] = fma(-acc[a2][jc], acc[b2][jc], acc[a2][b2]);
+                        }
+                    }
                 }
-                if (t == 0) {
-                    s_dmax = fmax(s_dmax, fabs(p));
-                    s_dmin = fmin(s_dmin, p);
-                }
-                if (own && (tk > jt || (tk == jt && jc < 7))) {
-                    const double pinv = fb_rcp(p);
-                    double ci[8], ck[8];
+                s_dmax = dmax;
+                s_dmin = dmin;
+                if (bad) s_bad = 1;
 #pragma unroll
-                    for (int a = 0; a < 8; ++a) {
-                        ci[a] = col[9 * ti + a];
-                        ck[a] = col[9 * tk + a] * pinv;
+                for (int c2 = 0; c2 < 8; ++c2)
+#pragma unroll
+                    for (int a2 = 0; a2 < 8; ++a2) lp[c2 * CBP + 10 * jt + a2] = a2 >= c2 ? acc[a2][c2] : 0.0;
+                if (jt == LT)  // all 8 diagonal entries (a runtime register index would spill acc)
+#pragma unroll
+                    for (int a2 = 0; a2 < 8; ++a2) s_corner[a2] = acc[a2][a2];
+            }
+            __syncthreads();
+            if (s_bad || jt == LT) break;  // uniform
+            if (own && tk == jt && ti > jt) {
+                // forward substitution against L_jj^T, column by column, in place
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    const double r = rdiag[c2];
+#pragma unroll
+                    for (int a2 = 0; a2 < 8; ++a2) {
+                        double v = acc[a2][c2];
+#pragma unroll
+                        for (int b2 = 0; b2 < c2; ++b2) v = fma(-acc[a2][b2], lp[b2 * CBP + 10 * jt + c2], v);
+                        acc[a2][c2] = v * r;
+                    }
+                }
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2)
+#pragma unroll
+                    for (int a2 = 0; a2 < 8; ++a2) lp[c2 * CBP + 10 * ti + a2] = acc[a2][c2];
+            }
+            __syncthreads();
+            if (own && tk > jt) {
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    double li[8], lk[8];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const double2 x2 = *reinterpret_cast<const double2*>(lp + c2 * CBP + 10 * ti + 2 * h);
+                        const double2 y2 = *reinterpret_cast<const double2*>(lp + c2 * CBP + 10 * tk + 2 * h);
+                        li[2 * h] = x2.x;
+                        li[2 * h + 1] = x2.y;
+                        lk[2 * h] = y2.x;
+                        lk[2 * h + 1] = y2.y;
                     }
 #pragma unroll
-                    for (int a = 0; a < 8; ++a)
+                    for (int a2 = 0; a2 < 8; ++a2)
 #pragma unroll
-                        for (int b = 0; b < 8; ++b)
-                            if (tk > jt || b > jc) acc[a][b] = fma(-ci[a], ck[b], acc[a][b]);
+                        for (int b2 = 0; b2 < 8; ++b2) acc[a2][b2] = fma(-li[a2], lk[b2], acc[a2][b2]);
                 }
             }
         }
-        // Schur complement of the border corner
-        if (own && ti == (L >> 3) && tk == ti)
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int b = 0; b < 8; ++b)
-                    if (8 * ti + a == L && 8 * tk + b == L) s_piv = acc[a][b];
         __syncthreads();
         FB_MARK(3);
         if (t == 0) {
@@ -549,7 +599,7 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
                 atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
                                         HSAD_E_SINGULAR_AFTER_RIDGE);
             } else {
-                score = -s_piv;
+                score = -s_corner[L & 7];
                 if (!isfinite(score)) {
                     atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
                                             (HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
@@ -591,8 +641,8 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
         // register-resident tiles: shared memory holds only samples and vectors
         P.mp = mp8;
         P.chunk = 32;
-        const size_t smem =
-            (static_cast<size_t>(P.chunk) * (P.mp / 8) * 10 + 3 * P.mp + 2 * (P.mp / 8) * 9 + nsamp) * 8;
+        const size_t smem = (static_cast<size_t>(P.chunk) * (P.mp / 8) * 10 + 3 * P.mp +
+                             2 * (8 * (P.mp / 8) * 10 + 8) + nsamp) * 8;
         HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_reg_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
