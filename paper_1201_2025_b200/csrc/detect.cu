@@ -84,6 +84,7 @@ struct DetectParams {
     int nreq;
     ReqDev req[kMaxRequests];
     int std_layout;  // box 0 = LRX/outer window for every request, box 1 = inner box
+    int staged;      // STD kernel: the update rows arrive in shared memory by TMA bulk copies
     int has_dual;
     double n_in, n_ann;  // standard-layout dual counts
     unsigned long long* status;
@@ -705,6 +706,7 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
     constexpr int S2 = Dim<L>::S2;
     extern __shared__ double2 s_v2[];
     __shared__ ReqDev s_req[kMaxRequests];
+    __shared__ uint64_t s_bar;  // STD: stage-full barrier of the row-update copies
 
     const int t = threadIdx.x;
     const int NT = blockDim.x;
@@ -742,6 +744,39 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
         for (int i = 0; i < L; ++i) y[i] -= shift[i];
     };
 
+    // STD (fp64 cube): the entering and leaving rows of every box for the update of
+    // row rr are copied by one thread with TMA bulk copies (cp.async.bulk, one per
+    // row: the strip's clipped column range is contiguous in BIP) into a shared
+    // stage while the CTA still solves row rr - 1, so the update reads shared
+    // memory instead of waiting on L2/HBM. stage[(2k + dir) * ncol + col][L].
+    const int64_t st_lo = c0 - P.rmax > 0 ? c0 - P.rmax : 0;
+    const int64_t st_hi = c0 + P.tw + P.rmax < P.samples ? c0 + P.tw + P.rmax : P.samples;
+    double* stage = reinterpret_cast<double*>(s_v2 + NBOX * box_stride);
+    auto issue_rows = [&](int64_t rr) {  // thread 0 only
+        const uint32_t seg = static_cast<uint32_t>((st_hi - st_lo) * L * sizeof(double));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&s_bar, seg * 2 * NBOX);
+#pragma unroll
+        for (int k = 0; k < NBOX; ++k) {
+            const int R = P.radius[k];
+#pragma unroll
+            for (int dir = 0; dir < 2; ++dir) {
+                const int vrow = static_cast<int>(dir == 0 ? rr + R : rr - 1 - R);
+                const int64_t drow = mirror32(vrow, static_cast<int>(P.lines)) - P.buf_row0;
+                const double* src = static_cast<const double*>(P.cube) + (drow * P.samples + st_lo) * L;
+                bulk_g2s(stage + static_cast<int64_t>(2 * k + dir) * ncol * L, src, seg, &s_bar);
+            }
+        }
+    };
+    uint32_t st_phase = 0;
+    if constexpr (STD) {
+        if (t == 0) {
+            mbar_init(&s_bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            if (ra + 1 < rb) issue_rows(ra + 1);
+        }
+    }
+
     // initial vertical sums over rows [ra - R_k, ra + R_k]
     for (int c = t; c < ncol; c += NT) {
         const char* cb = colbase_of(c);
@@ -773,14 +808,40 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
         double yc1[L];
         if (owner1) shifted(own_cb, r, yc1);
         if (r > ra) {
+            if constexpr (STD) {
+                mbar_wait(&s_bar, st_phase);
+                st_phase ^= 1;
+            }
             for (int c = t; c < ncol; c += NT) {
                 const char* cb = colbase_of(c);
+                // stage column of strip column c: every column a valid output's window
+                // reads mirrors into [lo, hi); the clamp only guards the unused tail
+                // columns of a strip that runs past the image
+                const int scol = min(max(mirror32(static_cast<int>(c0 - P.rmax + c),
+                                                  static_cast<int>(P.samples)) -
+                                             static_cast<int>(st_lo),
+                                         0),
+                                     static_cast<int>(st_hi - st_lo) - 1);
 #pragma unroll
                 for (int k = 0; k < NBOX; ++k) {
                     const int R = P.radius[k];
                     double yin[L], yout[L], dm[NC];
-                    shifted(cb, r + R, yin);
-                    shifted(cb, r - 1 - R, yout);
+                    if constexpr (STD) {
+                        const double* si = stage + (static_cast<int64_t>(2 * k) * ncol + scol) * L;
+                        const double* so = si + static_cast<int64_t>(ncol) * L;
+#pragma unroll
+                        for (int i = 0; i < L; i += 2) {
+                            const double2 a = *reinterpret_cast<const double2*>(si + i);
+                            const double2 b = *reinterpret_cast<const double2*>(so + i);
+                            yin[i] = a.x - shift[i];
+                            yin[i + 1] = a.y - shift[i + 1];
+                            yout[i] = b.x - shift[i];
+                            yout[i + 1] = b.y - shift[i + 1];
+                        }
+                    } else {
+                        shifted(cb, r + R, yin);
+                        shifted(cb, r - 1 - R, yout);
+                    }
 #pragma unroll
                     for (int i = 0; i < NC; ++i) dm[i] = 0.0;
                     add_moments<L>(dm, yin, 1.0);
@@ -798,6 +859,9 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
         }
         PT_MARK(0);  // vertical update
         __syncthreads();
+        if constexpr (STD) {  // the stage is consumed: fetch the next row's update rows
+            if (t == 0 && r > ra && r + 1 < rb) issue_rows(r + 1);  // ra + 1: issued at start
+        }
         PT_MARK(1);  // barrier A
         if (seg0 < P.tw && c0 + seg0 < P.samples) {
             double S[NBOX][NC];
@@ -854,12 +918,18 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
     PT_FLUSH();
 }
 
+// TMA row stage of the STD kernel: entering + leaving row of every box, strip width
+size_t stage_bytes(int nbox, int64_t ncol, int bands) {
+    return static_cast<size_t>(2 * nbox) * ncol * bands * sizeof(double);
+}
+
 template <int L, int NB>
 cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
     const int ncol = P.tw + 2 * P.rmax;
-    auto go = [&](auto kern, int K) -> cudaError_t {
+    auto go = [&](auto kern, int K, bool staged) -> cudaError_t {
         const size_t smem = static_cast<size_t>(NB) *
-                            (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)) * sizeof(double2);
+                                (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)) * sizeof(double2) +
+                            (staged ? stage_bytes(NB, ncol, L) : 0);
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
@@ -872,16 +942,16 @@ cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaS
         // kernel without the general box-selection path and the fp32 load path
         // (smaller code: fewer instruction-cache misses, measured -5% on C5)
         if constexpr (NB <= 2) {
-            if (P.std_layout && P.elem_bytes == 8) {
-                if (kcols == 4) return go(detect_kernel<L, NB, 4, true>, 4);
-                if (kcols == 2) return go(detect_kernel<L, NB, 2, true>, 2);
-                if (kcols == 1) return go(detect_kernel<L, NB, 1, true>, 1);
+            if (P.staged) {
+                if (kcols == 4) return go(detect_kernel<L, NB, 4, true>, 4, true);
+                if (kcols == 2) return go(detect_kernel<L, NB, 2, true>, 2, true);
+                if (kcols == 1) return go(detect_kernel<L, NB, 1, true>, 1, true);
             }
         }
-        if (kcols == 4) return go(detect_kernel<L, NB, 4, false>, 4);
-        if (kcols == 2) return go(detect_kernel<L, NB, 2, false>, 2);
+        if (kcols == 4) return go(detect_kernel<L, NB, 4, false>, 4, false);
+        if (kcols == 2) return go(detect_kernel<L, NB, 2, false>, 2, false);
     }
-    if (kcols == 1) return go(detect_kernel<L, NB, 1, false>, 1);
+    if (kcols == 1) return go(detect_kernel<L, NB, 1, false>, 1, false);
     return cudaErrorInvalidValue;
 }
 
@@ -1122,6 +1192,12 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     if (fullband) kc = 1;
     plan.kcols = kc;
     P.tw = 128 * kc;
+    // STD kernel (standard layout, fp64 4-band cube) with the TMA row stage, if the
+    // stage fits next to the window sums under the 4-CTA/SM budget
+    P.staged = P.std_layout && elem_bytes == 8 && bands == 4 && P.nbox <= 2 &&
+               smem_for(kc) + static_cast<int64_t>(stage_bytes(P.nbox, P.tw + 2 * P.rmax, bands)) <=
+                   smem_cap &&
+               !getenv("HSAD_NO_STAGE");
     P.diag_lin = -1;
     P.diag_out = nullptr;
     const int64_t strips = (samples + P.tw - 1) / P.tw;

@@ -9,11 +9,13 @@ import oracle
 
 dev = "cuda:0"
 W1, W2 = hs.WindowConfig.single, hs.WindowConfig.dual
-for shape, bands in (((23, 31), 4), ((6, 9), 4), ((40, 5), 3), ((130, 300), 4), ((7, 7), 8)):
+for shape, bands in (((23, 31), 4), ((6, 9), 4), ((40, 5), 3), ((130, 300), 4), ((7, 7), 8),
+                     ((70, 129), 4), ((33, 2100), 4)):
     cube = torch.as_tensor(oracle.port.random_cube(*shape, bands, 7)).to(dev)
     reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwrx", W2(5, 11)),
             hs.DetectRequest("dwest", W2(5, 11), eigcount=True), hs.DetectRequest("lrx", W1(9), guard=3)]
     hs.detect_multi(cube, reqs)
+    hs.detect_multi(cube, reqs[:3])  # standard layout: the TMA-staged kernel
     hs.detect_multi(cube.float(), reqs[:2])
 full = torch.as_tensor(oracle.port.random_cube(37, 45, 189, 9)).to(dev)
 for out_dtype in (torch.float64, torch.float32):

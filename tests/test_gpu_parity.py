@@ -611,3 +611,38 @@ def test_pipeline_host_sweep_equals_device_path(orc):
         assert torch.equal(a, b.cpu())
         if ac is not None:
             assert torch.equal(ac, bc.cpu())
+
+
+# ------------------------------------------------------------------ TMA-staged kernel
+
+
+@pytest.mark.parametrize("lines,samples", [(6, 9), (23, 31), (70, 129), (33, 300), (9, 2100)])
+def test_staged_kernel_bit_identical_and_oracle(orc, monkeypatch, lines, samples):
+    """The standard-layout fp64 kernel takes its update rows from a TMA bulk-copy
+    stage (strips clipped at the image edges, mirrored rows/columns): the maps must
+    equal the global-load kernel's bit for bit (HSAD_NO_STAGE) and match the oracle."""
+    cube = orc.port.random_cube(lines, samples, 4, 5000 + lines)
+    reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwrx", W2(5, 11)),
+            hs.DetectRequest("dwest", W2(5, 11), eigcount=True)]
+    staged = run(cube, reqs)
+    monkeypatch.setenv("HSAD_NO_STAGE", "1")
+    plain = run(cube, reqs)
+    for (a, ca), (b, cb) in zip(staged, plain):
+        assert np.array_equal(a, b)
+        assert (ca is None and cb is None) or np.array_equal(ca, cb)
+    assert max_rel_diff(staged[0][0], orc.port.local_rx(cube, 11)) < TOL64
+    assert max_rel_diff(staged[1][0], orc.port.dwrx(cube, 5, 11)) < TOL64
+    s, c = orc.port.dwest(cube, 5, 11)
+    assert max_rel_diff(staged[2][0], s) < TOL64 and np.array_equal(staged[2][1], c)
+
+
+@pytest.mark.parametrize("lines,samples", [(12, 600), (7, 2100)])
+def test_staged_kernel_multi_column(orc, monkeypatch, lines, samples):
+    """LRX alone fits two output columns per thread next to the stage (K = 2)."""
+    cube = orc.port.random_cube(lines, samples, 4, 6000 + lines)
+    reqs = [hs.DetectRequest("lrx", W1(11))]
+    staged = run(cube, reqs)
+    monkeypatch.setenv("HSAD_NO_STAGE", "1")
+    plain = run(cube, reqs)
+    assert np.array_equal(staged[0][0], plain[0][0])
+    assert max_rel_diff(staged[0][0], orc.port.local_rx(cube, 11)) < TOL64
