@@ -217,6 +217,68 @@ hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, int64_t sampl
                                const hsad_detect_request* host_requests, int32_t n_requests,
                                hsad_pixel_error* err, void* stream);
 
+/* ---- ENVI ingest --------------------------------------------- */
+typedef enum hsad_interleave { /* hsad::Interleave, cube.hpp:20 */
+    HSAD_BSQ = 0,
+    HSAD_BIL = 1,
+    HSAD_BIP = 2
+} hsad_interleave;
+
+typedef struct hsad_cube_header { /* hsad::CubeHeader, cube.hpp:26-37 */
+    int32_t samples, lines, bands;
+    int32_t interleave;     /* hsad_interleave */
+    int32_t data_type_code; /* 1=u8, 2=i16, 4=f32, 5=f64, 12=u16 */
+    int32_t byte_order;     /* 0 little-endian, 1 big-endian */
+} hsad_cube_header;
+
+/* Replaces hsad::read_cube (proj/core/src/cube.cpp:198-253): validate the header
+ * (cube.cpp:22-45), check raw_bytes == samples*lines*bands*element_size
+ * (SizeMismatch), decode every element (byte swap, widen) from the header's
+ * interleave into the BIP cube d_out (out_bytes 8 = the reference's fp64
+ * HyperCube; 4 = fp32, only for u8/i16/u16/f32 sources, which fp32 holds
+ * exactly), and reject non-finite values with NonFiniteValue
+ * "at (row=r, col=c, band=b)" for the first one in (row, col, band) order.
+ * d_raw, d_out: device pointers. Synchronous (the status is read back). */
+hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                           void* d_out, int32_t out_bytes, void* stream);
+
+/* ---- evaluation on device ------------------------------------ */
+typedef struct hsad_roc_summary {
+    uint64_t positives, negatives;
+    /* sum over (positive, negative) pairs of 2 [s_pos > s_neg] + [s_pos == s_neg]:
+     * the reference's exact integer AUC numerator (eval.cpp:33-46) */
+    uint64_t auc_twice_num;
+    double auc;         /* auc_twice_num / (2 positives negatives), eval.cpp:54-55 */
+    uint64_t distinct;  /* distinct score values = ROC points - 1 */
+} hsad_roc_summary;
+
+/* hsad::roc_curve's AUC (proj/core/src/eval.cpp:10-57) for n scores (score_bytes
+ * 8 or 4) and a 0/1 truth mask (nonzero = positive, synth.cpp:15-18), all on the
+ * device. DegenerateTruth when either class is empty. When d_far / d_td are
+ * non-null they receive the ROC points (distinct + 1 each, far/td as in
+ * eval.cpp:30-52: (0,0) first, one step per distinct score, descending). The
+ * points need a full sort of the scores (a device radix sort); the AUC alone
+ * sorts only the positives. Synchronous. */
+hsad_status hsad_roc(const void* d_scores, int32_t score_bytes, const uint8_t* d_truth, int64_t n,
+                     hsad_roc_summary* out, double* d_far, double* d_td, int64_t points_capacity,
+                     void* stream);
+
+/* Indices (ascending) of the k largest scores; ties at the k-th value are broken
+ * towards lower indices. *kth = the k-th largest score. Synchronous. */
+hsad_status hsad_top_k(const void* d_scores, int32_t score_bytes, int64_t n, int64_t k,
+                       int64_t* d_indices, double* kth, void* stream);
+
+/* hsad::adaptive_threshold (eval.cpp:69-90): tau = mean + z_alpha * sqrt(population
+ * variance) (two passes, fp64 with compensated per-thread sums), d_mask[i] =
+ * scores[i] > tau. InvalidValue on an empty map. Synchronous. */
+hsad_status hsad_adaptive_threshold(const void* d_scores, int32_t score_bytes, int64_t n,
+                                    double z_alpha, double* tau, uint8_t* d_mask, void* stream);
+
+/* hsad::render_pgm's pixel stretch (eval.cpp:92-109): lo/hi = min/max score,
+ * pixel = lround((s - lo) * (255 / (hi - lo))) when hi > lo, else 0. Synchronous. */
+hsad_status hsad_render_pgm(const void* d_scores, int32_t score_bytes, int64_t n,
+                            uint8_t* d_pixels, void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

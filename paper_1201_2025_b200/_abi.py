@@ -15,6 +15,8 @@ LIB_PATH = Path(os.environ.get("HSAD_B200_LIB", PKG / "libhsad_b200.so"))
 
 HSAD_OK = 0
 HSAD_E_INVALID_VALUE = 2
+HSAD_E_SIZE_MISMATCH = 3
+HSAD_E_NON_FINITE_VALUE = 4
 HSAD_E_OUT_OF_BOUNDS = 5
 HSAD_E_UNSUPPORTED_ORDER = 6
 HSAD_E_TOO_SHORT = 8
@@ -22,6 +24,8 @@ HSAD_E_TARGET_TOO_LARGE = 10
 HSAD_E_TOO_FEW_SAMPLES = 12
 HSAD_E_SINGULAR_AFTER_RIDGE = 13
 HSAD_E_CONFIG_MISMATCH = 16
+HSAD_E_DIMENSION_MISMATCH = 19
+HSAD_E_DEGENERATE_TRUTH = 20
 HSAD_E_CUDA = 64
 HSAD_E_UNSUPPORTED = 65
 
@@ -34,7 +38,10 @@ EXPORTED = [
     "hsad_device_check", "hsad_mirror_index", "hsad_window_validate", "hsad_daubechies_filters",
     "hsad_reduce", "hsad_detect", "hsad_detect_multi", "hsad_strip_rows", "hsad_row_quantum",
     "hsad_decode_status", "hsad_pipeline_host", "hsad_reduce_detect",
+    "hsad_read_cube", "hsad_roc", "hsad_top_k", "hsad_adaptive_threshold", "hsad_render_pgm",
 ]
+
+HSAD_BSQ, HSAD_BIL, HSAD_BIP = 0, 1, 2
 
 
 class Window(C.Structure):
@@ -51,6 +58,16 @@ class Request(C.Structure):
 
 class PixelError(C.Structure):
     _fields_ = [("code", C.c_int32), ("row", C.c_int64), ("col", C.c_int64)]
+
+
+class CubeHeader(C.Structure):  # hsad_cube_header
+    _fields_ = [("samples", C.c_int32), ("lines", C.c_int32), ("bands", C.c_int32),
+                ("interleave", C.c_int32), ("data_type_code", C.c_int32), ("byte_order", C.c_int32)]
+
+
+class RocSummary(C.Structure):  # hsad_roc_summary
+    _fields_ = [("positives", C.c_uint64), ("negatives", C.c_uint64),
+                ("auc_twice_num", C.c_uint64), ("auc", C.c_double), ("distinct", C.c_uint64)]
 
 
 class Limits(C.Structure):
@@ -87,6 +104,11 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
         "hsad_decode_status": (I32, [C.c_uint64, I64, P(PixelError)]),
         "hsad_pipeline_host": (I32, [VP, I64, I64, I32, I32, I32, P(Request), I32,
                                      P(PixelError), VP]),
+        "hsad_read_cube": (I32, [VP, I64, P(CubeHeader), VP, I32, VP]),
+        "hsad_roc": (I32, [VP, I32, VP, I64, P(RocSummary), VP, VP, I64, VP]),
+        "hsad_top_k": (I32, [VP, I32, I64, I64, VP, P(D), VP]),
+        "hsad_adaptive_threshold": (I32, [VP, I32, I64, D, P(D), VP, VP]),
+        "hsad_render_pgm": (I32, [VP, I32, I64, VP, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1,0 +1,217 @@
+// ENVI ingest on the device: hsad::read_cube (proj/core/src/cube.cpp:198-253).
+//
+// The reference decodes a raw ENVI cube element by element on the host: validate
+// the header (cube.cpp:22-45), check the byte count, then for every (row, col,
+// band) in that order read the source element from its interleave position
+// (BSQ band*plane + row*samples + col, BIL (row*bands + band)*samples + col, BIP
+// (row*samples + col)*bands + band), byte-swap if the file's byte order differs
+// from the host's, widen to fp64 and reject non-finite values.
+//
+// Here the raw file bytes are already in HBM and the whole decode is one
+// HBM-bound pass:
+//   * BSQ and BIL are batched (bands x columns) -> (columns x bands) transposes
+//     (BSQ: one batch of lines*samples columns; BIL: one batch per line), moved
+//     through 32 x 32 shared-memory tiles so both the band-plane reads and the
+//     BIP writes are coalesced;
+//   * BIP is a streaming element-wise decode;
+//   * typed, naturally aligned loads (u8/i16/u16/f32/f64), byte swap in
+//     registers (PRMT), widen to the output type (fp64 = the reference's
+//     HyperCube, or fp32 for sources fp32 holds exactly);
+//   * a non-finite value records its BIP linear index with atomicMin, so the
+//     error names the first one in the reference's (row, col, band) loop order.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "hsad_internal.h"
+
+namespace hsad_b200 {
+namespace {
+
+template <int CODE>
+struct Src;
+template <> struct Src<1> { using T = uint8_t; };
+template <> struct Src<2> { using T = uint16_t; };   // int16 bits
+template <> struct Src<4> { using T = uint32_t; };   // float bits
+template <> struct Src<5> { using T = uint64_t; };   // double bits
+template <> struct Src<12> { using T = uint16_t; };
+
+__device__ __forceinline__ uint16_t bswap16(uint16_t v) {
+    return static_cast<uint16_t>(__byte_perm(v, 0, 0x3201) & 0xffffu);
+}
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+__device__ __forceinline__ uint64_t bswap64(uint64_t v) {
+    const uint32_t lo = static_cast<uint32_t>(v), hi = static_cast<uint32_t>(v >> 32);
+    return (static_cast<uint64_t>(bswap32(lo)) << 32) | bswap32(hi);
+}
+
+// widen<T>(p, swap), cube.cpp:214-224
+template <int CODE>
+__device__ __forceinline__ double decode(typename Src<CODE>::T raw, bool swap) {
+    if constexpr (CODE == 1) {
+        return static_cast<double>(raw);
+    } else if constexpr (CODE == 2) {
+        return static_cast<double>(static_cast<int16_t>(swap ? bswap16(raw) : raw));
+    } else if constexpr (CODE == 12) {
+        return static_cast<double>(swap ? bswap16(raw) : raw);
+    } else if constexpr (CODE == 4) {
+        return static_cast<double>(__uint_as_float(swap ? bswap32(raw) : raw));
+    } else {
+        return __longlong_as_double(static_cast<long long>(swap ? bswap64(raw) : raw));
+    }
+}
+
+template <int CODE>
+__device__ __forceinline__ void check_finite(double v, int64_t bip_index, unsigned long long* status) {
+    if constexpr (CODE == 4 || CODE == 5) {
+        if (!isfinite(v)) atomicMin(status, static_cast<unsigned long long>(bip_index));
+    }
+}
+
+constexpr int kTile = 32;
+constexpr int kRowsPerPass = 8;
+
+// Batched transpose: in[batch][r][c] (r < R bands, c < C columns) -> out[(batch*C + c)*R + r].
+template <int CODE, typename Tout>
+__global__ void __launch_bounds__(kTile * kRowsPerPass)
+    ingest_transpose_kernel(const typename Src<CODE>::T* __restrict__ in, bool swap, int R, int64_t C,
+                            Tout* __restrict__ out, unsigned long long* status) {
+    __shared__ Tout tile[kTile][kTile + 1];
+    const int64_t batch = blockIdx.z;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kTile;
+    const int r0 = blockIdx.y * kTile;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const typename Src<CODE>::T* src = in + batch * R * C;
+    // load: lanes along columns (contiguous in BSQ planes / BIL lines)
+#pragma unroll
+    for (int k = 0; k < kTile; k += kRowsPerPass) {
+        const int r = r0 + ty + k;
+        const int64_t c = c0 + tx;
+        if (r < R && c < C) {
+            const double v = decode<CODE>(__ldg(src + static_cast<int64_t>(r) * C + c), swap);
+            check_finite<CODE>(v, (batch * C + c) * R + r, status);
+            tile[ty + k][tx] = static_cast<Tout>(v);
+        }
+    }
+    __syncthreads();
+    // store: lanes along bands (contiguous in BIP)
+#pragma unroll
+    for (int k = 0; k < kTile; k += kRowsPerPass) {
+        const int64_t c = c0 + ty + k;
+        const int r = r0 + tx;
+        if (r < R && c < C) out[(batch * C + c) * R + r] = tile[tx][ty + k];
+    }
+}
+
+// BIP source: element-wise decode (grid-stride)
+template <int CODE, typename Tout>
+__global__ void ingest_bip_kernel(const typename Src<CODE>::T* __restrict__ in, bool swap, int64_t n,
+                                  Tout* __restrict__ out, unsigned long long* status) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = decode<CODE>(__ldg(in + i), swap);
+        check_finite<CODE>(v, i, status);
+        out[i] = static_cast<Tout>(v);
+    }
+}
+
+template <int CODE, typename Tout>
+cudaError_t launch_ingest(const hsad_cube_header& h, const void* raw, bool swap, void* out,
+                          unsigned long long* status, cudaStream_t s) {
+    using T = typename Src<CODE>::T;
+    const T* in = static_cast<const T*>(raw);
+    Tout* o = static_cast<Tout*>(out);
+    const int64_t plane = static_cast<int64_t>(h.lines) * h.samples;
+    if (h.interleave == HSAD_BIP) {
+        const int64_t n = plane * h.bands;
+        const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+        ingest_bip_kernel<CODE, Tout><<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, swap, n, o, status);
+        return cudaGetLastError();
+    }
+    const int64_t batches = h.interleave == HSAD_BSQ ? 1 : h.lines;
+    const int64_t C = h.interleave == HSAD_BSQ ? plane : h.samples;
+    const dim3 grid(static_cast<unsigned>((C + kTile - 1) / kTile),
+                    static_cast<unsigned>((h.bands + kTile - 1) / kTile), static_cast<unsigned>(batches));
+    if (grid.y > 65535 || grid.z > 65535) return cudaErrorInvalidConfiguration;
+    ingest_transpose_kernel<CODE, Tout><<<grid, dim3(kTile, kRowsPerPass), 0, s>>>(in, swap, h.bands, C, o,
+                                                                                  status);
+    return cudaGetLastError();
+}
+
+template <typename Tout>
+cudaError_t dispatch_code(const hsad_cube_header& h, const void* raw, bool swap, void* out,
+                          unsigned long long* status, cudaStream_t s) {
+    switch (h.data_type_code) {
+        case 1: return launch_ingest<1, Tout>(h, raw, swap, out, status, s);
+        case 2: return launch_ingest<2, Tout>(h, raw, swap, out, status, s);
+        case 4: return launch_ingest<4, Tout>(h, raw, swap, out, status, s);
+        case 5: return launch_ingest<5, Tout>(h, raw, swap, out, status, s);
+        case 12: return launch_ingest<12, Tout>(h, raw, swap, out, status, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int64_t element_size(int code) {  // cube.cpp:22-33
+    switch (code) {
+        case 1: return 1;
+        case 2: return 2;
+        case 4: return 4;
+        case 5: return 8;
+        case 12: return 2;
+    }
+    return 0;
+}
+
+}  // namespace
+}  // namespace hsad_b200
+
+using namespace hsad_b200;
+
+extern "C" hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                                      void* d_out, int32_t out_bytes, void* stream) {
+    if (!header) return set_error(HSAD_E_INVALID_VALUE, "null header");
+    const hsad_cube_header& h = *header;
+    // CubeHeader::validate (cube.cpp:39-45), same order and messages
+    if (h.samples < 1 || h.lines < 1 || h.bands < 1)
+        return set_error(HSAD_E_INVALID_VALUE, "samples, lines and bands must all be >= 1");
+    const int64_t esize = element_size(h.data_type_code);
+    if (esize == 0)
+        return set_error(HSAD_E_INVALID_VALUE,
+                         "unsupported data type code " + std::to_string(h.data_type_code));
+    if (h.byte_order != 0 && h.byte_order != 1)
+        return set_error(HSAD_E_INVALID_VALUE, "byte order must be 0 or 1");
+    if (h.interleave != HSAD_BSQ && h.interleave != HSAD_BIL && h.interleave != HSAD_BIP)
+        return set_error(HSAD_E_INVALID_VALUE, "unknown interleave " + std::to_string(h.interleave));
+    const int64_t expected = static_cast<int64_t>(h.samples) * h.lines * h.bands * esize;
+    if (raw_bytes != expected)  // cube.cpp:200-203
+        return set_error(HSAD_E_SIZE_MISMATCH, "raw data is " + std::to_string(raw_bytes) +
+                                                   " bytes, header expects " + std::to_string(expected));
+    if (out_bytes != 8 && out_bytes != 4)
+        return set_error(HSAD_E_INVALID_VALUE, "out_bytes must be 8 (fp64) or 4 (fp32)");
+    if (out_bytes == 4 && h.data_type_code == 5)
+        return set_error(HSAD_E_INVALID_VALUE,
+                         "an fp32 cube cannot hold an fp64 source exactly; use out_bytes 8");
+    if (!d_raw || !d_out) return set_error(HSAD_E_INVALID_VALUE, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // every supported host is little-endian: swap when the file is big-endian (cube.cpp:205)
+    const bool swap = h.byte_order == 1;
+    unsigned long long* status = nullptr;
+    HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
+    HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
+    cudaError_t e = out_bytes == 8 ? dispatch_code<double>(h, d_raw, swap, d_out, status, s)
+                                   : dispatch_code<float>(h, d_raw, swap, d_out, status, s);
+    unsigned long long first = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&first, status, sizeof(first), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(status, s);
+    if (e != cudaSuccess) return cuda_fail(e, "hsad_read_cube");
+    if (first != ~0ull) {  // cube.cpp:244-247
+        const int64_t band = static_cast<int64_t>(first % h.bands);
+        const int64_t pix = static_cast<int64_t>(first / h.bands);
+        return set_error(HSAD_E_NON_FINITE_VALUE, "at (row=" + std::to_string(pix / h.samples) +
+                                                      ", col=" + std::to_string(pix % h.samples) +
+                                                      ", band=" + std::to_string(band) + ")");
+    }
+    return HSAD_OK;
+}

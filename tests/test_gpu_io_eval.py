@@ -1,0 +1,142 @@
+"""GPU parity of the ingest / evaluation kernels (csrc/ingest.cu, csrc/eval.cu)
+against the reference's own cube.cpp / eval.cpp / pgm.cpp (oracle/_ref) and the
+numpy restatement (oracle/io_eval.py). Integer / byte work: bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import io_eval as io  # noqa: E402
+
+hs = pytest.importorskip("paper_1201_2025_b200")
+from paper_1201_2025_b200 import evalio  # noqa: E402
+from paper_1201_2025_b200.hsad import HsadError  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def refio_or_port():
+    return io.ref_io()
+
+
+def _raw(rng, lines, samples, bands, code, byte_order):
+    dt = {1: np.uint8, 2: np.int16, 4: np.float32, 5: np.float64, 12: np.uint16}[code]
+    if code in (4, 5):
+        v = rng.normal(0.0, 3.0, size=lines * samples * bands)
+    else:
+        info = np.iinfo(dt)
+        v = rng.integers(info.min, info.max, size=lines * samples * bands, endpoint=True)
+    return v.astype(np.dtype(dt).newbyteorder(">" if byte_order else "<")).tobytes()
+
+
+def _dev(raw: bytes):
+    return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(DEV)
+
+
+@pytest.mark.parametrize("interleave", ["bsq", "bil", "bip"])
+@pytest.mark.parametrize("code", [1, 2, 4, 5, 12])
+@pytest.mark.parametrize("byte_order", [0, 1])
+@pytest.mark.parametrize("shape", [(5, 7, 6), (33, 70, 189), (3, 1, 40)])
+def test_read_cube_bit_exact(interleave, code, byte_order, shape):
+    lines, samples, bands = shape
+    rng = np.random.default_rng(code * 100 + byte_order * 10 + lines)
+    raw = _raw(rng, lines, samples, bands, code, byte_order)
+    want = io.read_cube(raw, samples, lines, bands, interleave, code, byte_order)
+    r = refio_or_port()
+    if r is not None and lines * samples * bands < 100000:
+        assert np.array_equal(r.read_cube(raw, samples, lines, bands, interleave, code, byte_order), want)
+    hdr = evalio.CubeHeader(samples, lines, bands, interleave, code, byte_order)
+    got = evalio.read_cube(_dev(raw), hdr).cpu().numpy()
+    assert np.array_equal(got, want)
+    if code != 5:  # fp32 holds u8/i16/u16/f32 exactly
+        got32 = evalio.read_cube(_dev(raw), hdr, out_dtype=torch.float32).cpu().numpy()
+        assert np.array_equal(got32.astype(np.float64), want)
+
+
+def test_read_cube_errors_match_reference():
+    z = np.zeros((2, 3, 4), np.float32)
+    z[1, 0, 1] = np.inf
+    z[0, 2, 3] = np.nan
+    hdr = evalio.CubeHeader(4, 3, 2, "bsq", 4, 0)
+    with pytest.raises(HsadError) as e:
+        evalio.read_cube(_dev(z.tobytes()), hdr)
+    assert str(e.value) == "NonFiniteValue: at (row=0, col=1, band=1)"
+    with pytest.raises(HsadError) as e:
+        evalio.read_cube(_dev(z.tobytes()[:-4]), hdr)
+    assert str(e.value) == "SizeMismatch: raw data is 92 bytes, header expects 96"
+
+
+def _st(rng, lines, samples, ties, rate=0.05):
+    s = rng.random((lines, samples))
+    if ties:
+        s = np.round(s * 20) / 20
+        s[0, 0] = -0.0
+        s[0, 1] = 0.0
+    t = (rng.random((lines, samples)) < rate).astype(np.uint8)
+    t[0, 0], t[-1, -1] = 1, 0
+    return s, t
+
+
+@pytest.mark.parametrize("lines,samples,ties,rate", [(30, 41, False, 0.05), (30, 41, True, 0.05),
+                                                     (200, 300, False, 0.002), (64, 64, True, 0.5),
+                                                     (1, 2, False, 0.5)])
+def test_roc_exact(lines, samples, ties, rate):
+    rng = np.random.default_rng(lines + samples + ties)
+    s, t = _st(rng, lines, samples, ties, rate)
+    far, td, a, num = io.roc_curve(s, t)
+    r = refio_or_port()
+    if r is not None:
+        f1, t1, a1 = r.roc_curve(s, t)
+        assert a1 == a and np.array_equal(f1, far) and np.array_equal(t1, td)
+    for dtype in (torch.float64, torch.float32):
+        sd = torch.as_tensor(s).to(DEV, dtype)
+        s_used = sd.double().cpu().numpy()
+        far2, td2, a2, num2 = io.roc_curve(s_used, t)
+        c = evalio.roc_curve(sd, torch.as_tensor(t).to(DEV))
+        assert c.auc_twice_num == num2 and c.auc == a2
+        assert np.array_equal(c.far.cpu().numpy(), far2) and np.array_equal(c.td.cpu().numpy(), td2)
+        c2 = evalio.roc_curve(sd, torch.as_tensor(t).to(DEV), points=False)
+        assert c2.auc == a2
+
+
+def test_roc_degenerate_and_dimension_errors():
+    s = torch.rand(4, 5, dtype=torch.float64, device=DEV)
+    with pytest.raises(HsadError) as e:
+        evalio.roc_curve(s, torch.zeros(4, 5, dtype=torch.uint8, device=DEV))
+    assert str(e.value) == "DegenerateTruth: truth mask must contain both classes"
+    with pytest.raises(HsadError) as e:
+        evalio.roc_curve(s, torch.zeros(5, 4, dtype=torch.uint8, device=DEV))
+    assert e.value.name == "DimensionMismatch"
+
+
+@pytest.mark.parametrize("n,k,ties", [(1000, 1, False), (1000, 37, False), (5000, 500, True),
+                                      (100000, 100, False), (257, 257, True)])
+def test_top_k_set(n, k, ties):
+    rng = np.random.default_rng(n + k)
+    s = rng.random(n)
+    if ties:
+        s = np.round(s * 10) / 10
+    order = np.lexsort((np.arange(n), -s))  # score descending, index ascending
+    want = np.sort(order[:k])
+    idx, kth = evalio.top_k(torch.as_tensor(s).to(DEV), k)
+    assert np.array_equal(idx.cpu().numpy(), want)
+    assert kth == s[order[k - 1]]
+
+
+def test_threshold_and_pgm():
+    rng = np.random.default_rng(5)
+    s = rng.gamma(2.0, 1.5, size=(97, 131))
+    r = refio_or_port()
+    for z in (0.0, 2.0, 3.5):
+        tau_want, mask_want = (r.adaptive_threshold(s, z) if r is not None else io.adaptive_threshold(s, z))
+        res = evalio.adaptive_threshold(torch.as_tensor(s).to(DEV), z)
+        # compensated device sums vs the reference's sequential ones: rounding-level tau
+        assert abs(res.tau - tau_want) <= 1e-13 * abs(tau_want)
+        m = res.mask.cpu().numpy().ravel()
+        near = np.abs(s.ravel() - tau_want) <= 1e-12 * abs(tau_want)
+        assert np.array_equal(m[~near], mask_want[~near])
+    want = r.render_pgm(s) if r is not None else io.render_pgm(s)
+    assert evalio.render_pgm(torch.as_tensor(s).to(DEV)) == want
+    c = torch.full((3, 4), 2.5, dtype=torch.float64, device=DEV)
+    assert evalio.render_pgm(c) == io.render_pgm(np.full((3, 4), 2.5))
