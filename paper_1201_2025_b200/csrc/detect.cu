@@ -178,7 +178,7 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 // fp64 reciprocal with one Newton step (~2^-44 relative): enough where the result
 // only scales a correction that is itself ~1e-4 of its operand (polish angles)
-[[maybe_unused]] __device__ __forceinline__ double rcp1(double x) {
+__device__ __forceinline__ double rcp1(double x) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     return fma(y, fma(-x, y, 1.0), y);
@@ -375,11 +375,7 @@ __device__ __forceinline__ void sweep64(double (&a)[L][L], double (&v)[L][L]) {
         const bool small = fabs(apq) < 1e-4 * fabs(h) || apq == 0.0;
         double t, c;
         if (__all_sync(__activemask(), small)) {
-#ifdef HSAD_POLISH_RCP1
-            const double x = apq == 0.0 ? 0.0 : apq * rcp1(h);
-#else
-            const double x = apq == 0.0 ? 0.0 : apq * fast_rcp(h);
-#endif
+            const double x = apq == 0.0 ? 0.0 : apq * rcp1(h);  // 1 Newton step suffices here
             t = x * fma(-x, x, 1.0);
             c = fma(-0.5 * t, t, 1.0);
         } else {

@@ -104,6 +104,69 @@ __global__ void __launch_bounds__(kTile * kRowsPerPass)
     }
 }
 
+// Whole-spectrum tiles: one CTA moves PIX consecutive columns x all R bands, so the
+// BIP output of the tile is one contiguous R*PIX run (fully coalesced writes) and
+// every band row is read as one PIX-column segment (128 B for u8..f32 sources at
+// PIX = 32). Loads are issued U bands at a time per warp so enough bytes are in
+// flight to cover HBM latency. Used when the tile fits in shared memory.
+constexpr int kWideThreads = 256;
+constexpr int kWideWarps = kWideThreads / 32;
+template <typename Tout>
+__host__ __device__ constexpr int wide_pix() { return sizeof(Tout) == 4 ? 64 : 32; }
+template <int CODE, typename Tout>
+__global__ void __launch_bounds__(kWideThreads)
+    ingest_wide_kernel(const typename Src<CODE>::T* __restrict__ in, bool swap, int R, int64_t C,
+                       Tout* __restrict__ out, unsigned long long* status) {
+    using T = typename Src<CODE>::T;
+    constexpr int PIX = wide_pix<Tout>();
+    constexpr int CPL = PIX / 32;  // columns per lane
+    constexpr int U = sizeof(Tout) == 4 ? 8 : 14;  // band rows in flight per warp (measured)
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    Tout* tile = reinterpret_cast<Tout*>(s_raw);  // [PIX][R + 1]
+    const int stride = R + 1;
+    const int64_t batch = blockIdx.y;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * PIX;
+    const int ncol = static_cast<int>(C - c0 < PIX ? C - c0 : PIX);
+    const T* src = in + batch * R * C + c0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int b0 = warp; b0 < R; b0 += kWideWarps * U) {
+        T raw[U][CPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+                const int b = b0 + u * kWideWarps, c = lane + 32 * j;
+                raw[u][j] = (b < R && c < ncol) ? __ldg(src + static_cast<int64_t>(b) * C + c) : T(0);
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+                const int b = b0 + u * kWideWarps, c = lane + 32 * j;
+                if (b < R && c < ncol) {
+                    const double v = decode<CODE>(raw[u][j], swap);
+                    check_finite<CODE>(v, (batch * C + c0 + c) * R + b, status);
+                    tile[c * stride + b] = static_cast<Tout>(v);
+                }
+            }
+    }
+    __syncthreads();
+    // store: the tile's BIP run [(batch*C + c0) * R, + ncol * R) in order
+    Tout* dst = out + (batch * C + c0) * R;
+    const int total = ncol * R;
+    int c = threadIdx.x / R, b = threadIdx.x % R;
+    const int dc = kWideThreads / R, db = kWideThreads % R;
+    for (int i = threadIdx.x; i < total; i += kWideThreads) {
+        dst[i] = tile[c * stride + b];
+        c += dc;
+        b += db;
+        if (b >= R) {
+            b -= R;
+            ++c;
+        }
+    }
+}
+
 // BIP source: element-wise decode (grid-stride)
 template <int CODE, typename Tout>
 __global__ void ingest_bip_kernel(const typename Src<CODE>::T* __restrict__ in, bool swap, int64_t n,
@@ -131,6 +194,17 @@ cudaError_t launch_ingest(const hsad_cube_header& h, const void* raw, bool swap,
     }
     const int64_t batches = h.interleave == HSAD_BSQ ? 1 : h.lines;
     const int64_t C = h.interleave == HSAD_BSQ ? plane : h.samples;
+    const size_t wide_smem = static_cast<size_t>(wide_pix<Tout>()) * (h.bands + 1) * sizeof(Tout);
+    if (wide_smem <= 100 * 1024 && batches <= 65535) {
+        auto kern = ingest_wide_kernel<CODE, Tout>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(wide_smem));
+        if (e != cudaSuccess) return e;
+        const dim3 g(static_cast<unsigned>((C + wide_pix<Tout>() - 1) / wide_pix<Tout>()),
+                     static_cast<unsigned>(batches));
+        kern<<<g, kWideThreads, wide_smem, s>>>(in, swap, h.bands, C, o, status);
+        return cudaGetLastError();
+    }
     const dim3 grid(static_cast<unsigned>((C + kTile - 1) / kTile),
                     static_cast<unsigned>((h.bands + kTile - 1) / kTile), static_cast<unsigned>(batches));
     if (grid.y > 65535 || grid.z > 65535) return cudaErrorInvalidConfiguration;
