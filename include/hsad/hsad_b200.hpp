@@ -71,10 +71,16 @@ struct DeviceBuffer {
 };
 }  // namespace detail
 
+enum class Interleave { BSQ, BIL, BIP };  // cube.hpp:20
+
+/// ENVI raster header (cube.hpp:26-37); data_type_code 1=u8, 2=i16, 4=f32, 5=f64, 12=u16.
 struct CubeHeader {
     int samples = 0;
     int lines = 0;
     int bands = 0;
+    Interleave interleave = Interleave::BSQ;
+    int data_type_code = 5;
+    int byte_order = 0;
 };
 
 /// fp64 cube, (row, col, band) with band fastest (cube.hpp:39-64).
@@ -284,6 +290,118 @@ inline ScoreMap detect(const HyperCube& cube, Algorithm algo, const WindowConfig
         case Algorithm::DWEST: return dwest(cube, config, options.dwest, options.workers);
     }
     throw Error(errc::invalid_value, "InvalidValue: unknown algorithm");
+}
+
+// ---- ENVI decode and evaluation (cube.hpp:70-72, eval.hpp:14-45) ---------------------
+
+struct GroundTruthMask {
+    int lines = 0;
+    int samples = 0;
+    std::vector<std::uint8_t> mask;  ///< row-major, 0 or 1
+};
+
+/// read_cube (cube.cpp:198-253): raw ENVI bytes -> fp64 BIP cube, decoded on the GPU.
+inline HyperCube read_cube(const CubeHeader& header, const std::uint8_t* raw, size_t raw_bytes) {
+    using namespace detail;
+    hsad_cube_header h{header.samples, header.lines, header.bands,
+                       static_cast<int32_t>(header.interleave), header.data_type_code, header.byte_order};
+    const size_t n = header.samples > 0 && header.lines > 0 && header.bands > 0
+                         ? static_cast<size_t>(header.samples) * header.lines * header.bands
+                         : 0;
+    DeviceBuffer draw(raw_bytes), dout(n * sizeof(double));
+    if (raw_bytes) cuda(cudaMemcpy(draw.p, raw, raw_bytes, cudaMemcpyHostToDevice), "H2D");
+    check(hsad_read_cube(draw.p, static_cast<int64_t>(raw_bytes), &h, dout.p, 8, nullptr));
+    HyperCube cube(header.lines, header.samples, header.bands);
+    cube.header = header;
+    cube.header.data_type_code = 5;
+    cube.header.byte_order = 0;
+    cuda(cudaMemcpy(cube.values.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    return cube;
+}
+
+struct RocPoint {
+    double far = 0.0;
+    double td = 0.0;
+};
+struct RocCurve {
+    std::vector<RocPoint> points;
+    double auc = 0.0;
+};
+
+/// roc_curve (eval.cpp:10-57): exact integer AUC and one point per distinct score.
+inline RocCurve roc_curve(const ScoreMap& scores, const GroundTruthMask& truth) {
+    using namespace detail;
+    if (scores.lines != truth.lines || scores.samples != truth.samples)
+        throw Error(errc::dimension_mismatch,
+                    "DimensionMismatch: score map is " + std::to_string(scores.lines) + "x" +
+                        std::to_string(scores.samples) + ", truth is " + std::to_string(truth.lines) +
+                        "x" + std::to_string(truth.samples));
+    const size_t n = scores.scores.size();
+    DeviceBuffer ds(n * sizeof(double)), dt(n), dfar((n + 1) * sizeof(double)), dtd((n + 1) * sizeof(double));
+    if (n) {
+        cuda(cudaMemcpy(ds.p, scores.scores.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        cuda(cudaMemcpy(dt.p, truth.mask.data(), n, cudaMemcpyHostToDevice), "H2D");
+    }
+    hsad_roc_summary sum{};
+    check(hsad_roc(ds.p, 8, static_cast<const uint8_t*>(dt.p), static_cast<int64_t>(n), &sum,
+                   static_cast<double*>(dfar.p), static_cast<double*>(dtd.p), static_cast<int64_t>(n + 1),
+                   nullptr));
+    const size_t np = static_cast<size_t>(sum.distinct) + 1;
+    std::vector<double> far(np), td(np);
+    cuda(cudaMemcpy(far.data(), dfar.p, np * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cuda(cudaMemcpy(td.data(), dtd.p, np * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    RocCurve c;
+    c.points.resize(np);
+    for (size_t i = 0; i < np; ++i) c.points[i] = {far[i], td[i]};
+    c.auc = sum.auc;
+    return c;
+}
+
+/// auc (eval.cpp:59-67): trapezoidal area under the points.
+inline double auc(const RocCurve& curve) {
+    double area = 0.0;
+    for (size_t i = 1; i < curve.points.size(); ++i)
+        area += (curve.points[i].far - curve.points[i - 1].far) *
+                (curve.points[i - 1].td + curve.points[i].td) / 2.0;
+    return area;
+}
+
+struct ThresholdResult {
+    double tau = 0.0;
+    GroundTruthMask mask;
+    double z_alpha = 0.0;
+};
+
+/// adaptive_threshold (eval.cpp:69-90) on the GPU.
+inline ThresholdResult adaptive_threshold(const ScoreMap& scores, double z_alpha) {
+    using namespace detail;
+    const size_t n = scores.scores.size();
+    DeviceBuffer ds(n * sizeof(double)), dm(n);
+    if (n) cuda(cudaMemcpy(ds.p, scores.scores.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    ThresholdResult r;
+    r.z_alpha = z_alpha;
+    check(hsad_adaptive_threshold(ds.p, 8, static_cast<int64_t>(n), z_alpha, &r.tau,
+                                  static_cast<uint8_t*>(dm.p), nullptr));
+    r.mask.lines = scores.lines;
+    r.mask.samples = scores.samples;
+    r.mask.mask.resize(n);
+    cuda(cudaMemcpy(r.mask.mask.data(), dm.p, n, cudaMemcpyDeviceToHost), "D2H");
+    return r;
+}
+
+/// render_pgm (eval.cpp:92-109): complete binary PGM bytes.
+inline std::vector<std::uint8_t> render_pgm(const ScoreMap& scores) {
+    using namespace detail;
+    const size_t n = scores.scores.size();
+    DeviceBuffer ds(n * sizeof(double)), dp(n);
+    if (n) cuda(cudaMemcpy(ds.p, scores.scores.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    check(hsad_render_pgm(ds.p, 8, static_cast<int64_t>(n), static_cast<uint8_t*>(dp.p), nullptr));
+    const std::string head =
+        "P5\n" + std::to_string(scores.samples) + " " + std::to_string(scores.lines) + "\n255\n";
+    std::vector<std::uint8_t> out(head.begin(), head.end());
+    out.resize(head.size() + n);
+    if (n) cuda(cudaMemcpy(out.data() + head.size(), dp.p, n, cudaMemcpyDeviceToHost), "D2H");
+    return out;
 }
 
 }  // namespace hsad

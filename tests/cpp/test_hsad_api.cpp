@@ -153,6 +153,58 @@ int main() {
                  std::string(e.what()).find("at pixel (2, 2)") != std::string::npos;
     }
     CHECK(msg_ok);
+    // ENVI decode (cube.cpp:198-253): a 2x3x2 big-endian int16 BIL cube
+    {
+        CubeHeader h;
+        h.lines = 2;
+        h.samples = 3;
+        h.bands = 2;
+        h.interleave = Interleave::BIL;
+        h.data_type_code = 2;
+        h.byte_order = 1;
+        std::vector<std::uint8_t> raw;
+        for (int row = 0; row < 2; ++row)
+            for (int b = 0; b < 2; ++b)
+                for (int c = 0; c < 3; ++c) {
+                    const int16_t v = static_cast<int16_t>(-100 * row + 10 * b + c);
+                    raw.push_back(static_cast<std::uint8_t>((v >> 8) & 0xff));
+                    raw.push_back(static_cast<std::uint8_t>(v & 0xff));
+                }
+        auto cube = read_cube(h, raw.data(), raw.size());
+        bool ok = true;
+        for (int row = 0; row < 2; ++row)
+            for (int c = 0; c < 3; ++c)
+                for (int b = 0; b < 2; ++b) ok = ok && cube.at(row, c, b) == -100.0 * row + 10 * b + c;
+        CHECK(ok);
+        CHECK_THROWS_CODE(read_cube(h, raw.data(), raw.size() - 2), errc::size_mismatch);
+        h.data_type_code = 4;
+        h.byte_order = 0;
+        std::vector<float> f32(12, 1.0f);
+        f32[7] = NAN;
+        CHECK_THROWS_CODE(read_cube(h, reinterpret_cast<const std::uint8_t*>(f32.data()), 48),
+                          errc::non_finite_value);
+    }
+    // ROC (eval.cpp:10-57): positives {0.9, 0.7}, negatives {0.8, 0.6} -> 3 of 4 pairs won
+    {
+        ScoreMap m;
+        m.lines = 1;
+        m.samples = 4;
+        m.scores = {0.9, 0.8, 0.7, 0.6};
+        GroundTruthMask t;
+        t.lines = 1;
+        t.samples = 4;
+        t.mask = {1, 0, 1, 0};
+        auto c = roc_curve(m, t);
+        CHECK(c.auc == 0.75 && c.points.size() == 5);
+        CHECK(c.points[1].far == 0.0 && c.points[1].td == 0.5 && c.points[2].far == 0.5);
+        CHECK(std::abs(auc(c) - 0.75) < 1e-15);
+        t.mask = {0, 0, 0, 0};
+        CHECK_THROWS_CODE(roc_curve(m, t), errc::degenerate_truth);
+        auto th = adaptive_threshold(m, 1.0);
+        CHECK(std::abs(th.tau - (0.75 + std::sqrt(0.0125))) < 1e-12 && th.mask.mask[0] == 1 && th.mask.mask[1] == 0);
+        auto pgm = render_pgm(m);
+        CHECK(pgm.size() == 11 + 4 && pgm[11] == 255 && pgm[14] == 0 && pgm[12] == 170);
+    }
     std::printf("cpp drop-in: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }
