@@ -377,7 +377,7 @@ def run_b200(args, cfg, rank, world, local, dist):
     step_gbs = value * 1e6 * bpp / 1e9
     # DRAM traffic per launch from the committed ncu --set full capture of this workload
     traffic, traffic_src = None, None
-    tfile = ROOT / "profiles" / "ncu_traffic_r1_sweep.json"
+    tfile = ROOT / "profiles" / "ncu_traffic_r1_sweep_b.json"
     if args.config == "C5" and world == 1 and tfile.exists():
         tj = json.loads(tfile.read_text())
         traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in tj["launches"]) / 1e9
