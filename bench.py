@@ -17,8 +17,9 @@ One step = one pass of that hot path over the cube:
           three streams, so the kernels and the D2H overlap the PCIe H2D).
 Multi-GPU (torchrun): row strips aligned to hsad_row_quantum, each rank holds its
 strip + mirror halo (generated from the same seeded row chunks = the host copy),
-computes it, and the fp64 maps are gathered to rank 0 with NCCL (dist.gather)
-inside the timed region. scaling = "strong" (the 4096^2 image is fixed).
+computes it, and the maps are gathered to rank 0 with NCCL (asynchronous dist.gather
+per window-pair group, so a group's maps travel while the next group's detectors run;
+sharded.MapGather) inside the timed region. scaling = "strong" (the 4096^2 image is fixed).
 
 --impl reference times the CPU restatement of the reference (oracle/, the
 reference itself needs Eigen3, absent here) on the host cores, rank 0 only.
@@ -259,21 +260,27 @@ def run_b200(args, cfg, rank, world, local, dist):
     q, per, r0, r1, b0, nb = plan.quantum, plan.per, plan.r0, plan.r1, plan.b0, plan.nb
     cube = generate_rows(lines, samples, bands, cfg["seed"], b0, b0 + nb, cfg["rate"], device=dev)
     red = torch.empty((nb, samples, 4), dtype=torch.float64, device=dev)
-    outs = [(torch.empty((r1 - r0, samples), dtype=torch.float64, device=dev),
-             torch.empty((r1 - r0, samples), dtype=torch.int8, device=dev) if r.eigcount else None)
-            for r in reqs]
+    # maps live in padded (per, samples) buffers: the strip's rows come first, so at N > 1
+    # they are the NCCL send buffers themselves (no staging copy)
+    from paper_1201_2025_b200.sharded import MapGather
+    gather = MapGather(plan, dist) if world > 1 else None
+    pad = lambda dt: torch.zeros((max(per, r1 - r0), samples), dtype=dt, device=dev)  # noqa: E731
+    outs_pad = [(pad(torch.float64), pad(torch.int8) if r.eigcount else None) for r in reqs]
+    outs = [(sc[: r1 - r0], None if cnt is None else cnt[: r1 - r0]) for sc, cnt in outs_pad]
     status = torch.full((1,), -1, dtype=torch.int64, device=dev)
-    gathered = None
-    if world > 1 and rank == 0:
-        gathered = [[torch.empty((per, samples), dtype=torch.float64, device=dev) for _ in range(world)]
-                    for _ in reqs]
-    send_bufs = [torch.zeros((per, samples), dtype=torch.float64, device=dev) for _ in reqs]
 
     lib = hs._abi.lib()
     import ctypes as C
     stream = torch.cuda.current_stream(dev)
-    creqs = (hs._abi.Request * len(reqs))(*[
-        hs.hsad._make_request(r, sc, cnt) for r, (sc, cnt) in zip(reqs, outs)])
+    # one request group per window pair of the sweep (3 requests: one fused launch each),
+    # so at N > 1 the maps of a finished group are gathered while the next group computes
+    per_group = len(reqs) // len(SWEEP)
+    groups = []
+    for g in range(len(SWEEP)):
+        sl = slice(g * per_group, (g + 1) * per_group)
+        groups.append(((hs._abi.Request * per_group)(*[
+            hs.hsad._make_request(r, sc, cnt) for r, (sc, cnt) in zip(reqs[sl], outs[sl])]),
+            list(range(sl.start, sl.stop))))
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     kern_ms = {"reduce": [], "detect": []}
 
@@ -283,15 +290,19 @@ def run_b200(args, cfg, rank, world, local, dist):
         assert st == 0, lib.hsad_last_error_message()
         if record:
             ev[1].record(stream)
-        st = lib.hsad_detect_multi(red.data_ptr(), 8, lines, samples, 4, b0, nb, r0, r1, creqs,
-                                   len(reqs), status.data_ptr(), None, stream.cuda_stream)
-        assert st == 0, lib.hsad_last_error_message()
+        for creqs, idx in groups:
+            st = lib.hsad_detect_multi(red.data_ptr(), 8, lines, samples, 4, b0, nb, r0, r1, creqs,
+                                       len(idx), status.data_ptr(), None, stream.cuda_stream)
+            assert st == 0, lib.hsad_last_error_message()
+            if gather is not None:  # NCCL gather of this group's maps, overlapping the next group
+                for i in idx:
+                    gather.launch(2 * i, outs_pad[i][0])
+                    if outs_pad[i][1] is not None:
+                        gather.launch(2 * i + 1, outs_pad[i][1])
         if record:
             ev[2].record(stream)
-        if world > 1:
-            for i, (sc, _) in enumerate(outs):
-                send_bufs[i][: r1 - r0].copy_(sc)
-                dist.gather(send_bufs[i], gathered[i] if rank == 0 else None, dst=0)
+        if gather is not None:
+            gather.wait()
 
     for _ in range(max(3, args.warmup)):
         step()

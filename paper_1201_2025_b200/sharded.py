@@ -57,18 +57,57 @@ def compute_strip_gpu(buf: torch.Tensor, plan: StripPlan, requests: Sequence[Det
                         row_begin=plan.r0, row_end=plan.r1, status=status)
 
 
+class MapGather:
+    """Gathers padded (per, samples) strip maps to rank `dst`, one asynchronous
+    dist.gather per map, so a group's maps travel while the next group of detectors
+    still computes (NCCL: the collective stream waits on the compute stream at launch,
+    the compute stream is free to run the next kernels; `wait()` joins them back).
+
+    Receive buffers are allocated once per map slot and reused across steps; the
+    full maps are views of them (rows [0, lines) of the concatenated strips)."""
+
+    def __init__(self, plan: StripPlan, dist, dst: int = 0):
+        self.plan, self.dist, self.dst = plan, dist, dst
+        self.recv: dict[int, torch.Tensor] = {}
+        self.works = []
+
+    def padded(self, dtype, device) -> torch.Tensor:
+        """A (per, samples) send buffer; the strip's rows are its first r1 - r0 rows."""
+        return torch.zeros((self.plan.per, self.plan.samples), dtype=dtype, device=device)
+
+    def launch(self, slot: int, send: torch.Tensor) -> None:
+        p = self.plan
+        if p.world == 1:
+            return
+        bufs = None
+        if p.rank == self.dst:
+            if slot not in self.recv:
+                self.recv[slot] = torch.empty((p.world * p.per, p.samples), dtype=send.dtype,
+                                              device=send.device)
+            bufs = list(self.recv[slot].split(p.per))
+        self.works.append(self.dist.gather(send, bufs, dst=self.dst, async_op=True))
+
+    def wait(self) -> None:
+        for w in self.works:
+            w.wait()
+        self.works.clear()
+
+    def full(self, slot: int) -> torch.Tensor | None:
+        if self.plan.rank != self.dst or slot not in self.recv:
+            return None
+        return self.recv[slot][: self.plan.lines]
+
+
 def gather_maps(maps: Sequence[torch.Tensor], plan: StripPlan, dist, dst: int = 0):
     """Gather each rank's [r1-r0, samples] map to rank `dst` (padded to plan.per rows).
     Returns the full [lines, samples] maps on dst, None elsewhere."""
-    out = []
-    for m in maps:
-        send = torch.zeros((plan.per, plan.samples), dtype=m.dtype, device=m.device)
+    g = MapGather(plan, dist, dst)
+    for i, m in enumerate(maps):
+        send = g.padded(m.dtype, m.device)
         send[: m.shape[0]].copy_(m)
-        bufs = ([torch.empty_like(send) for _ in range(plan.world)]
-                if plan.rank == dst else None)
-        dist.gather(send, bufs, dst=dst)
-        out.append(torch.cat(bufs)[: plan.lines] if plan.rank == dst else None)
-    return out
+        g.launch(i, send)
+    g.wait()
+    return [g.full(i) if plan.world > 1 else maps[i] for i in range(len(maps))]
 
 
 def run_sharded(rows_of: Callable[[int, int], torch.Tensor], lines: int, samples: int,

@@ -112,3 +112,71 @@ def test_sharded_gather_equals_single_process(orc, world):
     for (_, r0, r1, b0, nb) in plans:
         if r1 > r0:
             assert b0 <= max(0, r0 - 4) and b0 + nb >= min(LINES, r1 + 4)
+
+
+def _grouped_worker(rank, world, port, q):
+    """bench.py's N > 1 step: per window-pair group, the strip maps are written into
+    padded (per, samples) buffers and gathered asynchronously (sharded.MapGather)
+    while the next group computes; one wait at the end of the step."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1201_2025_b200 import DetectRequest, WindowConfig
+        from paper_1201_2025_b200.sharded import MapGather, plan_strip
+        cube = oracle.port.random_cube(LINES, SAMPLES, BANDS, 777)
+        sweep = [(3, 7), (5, 11)]
+        reqs = []
+        for i, o in sweep:
+            reqs += [DetectRequest("lrx", WindowConfig.single(o)),
+                     DetectRequest("dwest", WindowConfig.dual(i, o), eigcount=True)]
+        plan = plan_strip(LINES, SAMPLES, world, rank, reqs)
+        g = MapGather(plan, dist)
+        red = oracle.port.reduce_cube(cube, 2, 4)
+        rows = (plan.r0, plan.r1)
+        bufs = [(g.padded(torch.float64, "cpu"), g.padded(torch.int8, "cpu") if r.eigcount else None)
+                for r in reqs]
+        for step in range(2):  # receive buffers are reused across steps
+            for gi, (i, o) in enumerate(sweep):
+                s = oracle.port.local_rx(red, o, rows=rows)
+                bufs[2 * gi][0][: plan.r1 - plan.r0].copy_(torch.from_numpy(s))
+                ds, dc = oracle.port.dwest(red, i, o, rows=rows)
+                bufs[2 * gi + 1][0][: plan.r1 - plan.r0].copy_(torch.from_numpy(ds))
+                bufs[2 * gi + 1][1][: plan.r1 - plan.r0].copy_(torch.from_numpy(dc))
+                for k in (2 * gi, 2 * gi + 1):
+                    g.launch(2 * k, bufs[k][0])
+                    if bufs[k][1] is not None:
+                        g.launch(2 * k + 1, bufs[k][1])
+            g.wait()
+        if rank == 0:
+            q.put([g.full(2 * k).numpy().copy() for k in range(len(reqs))] +
+                  [g.full(3).numpy().copy(), g.full(7).numpy().copy()])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_grouped_async_gather_like_bench(orc, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grouped_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    got = q.get()
+    cube = orc.port.random_cube(LINES, SAMPLES, BANDS, 777)
+    red = orc.port.reduce_cube(cube, 2, 4)
+    want = []
+    counts = []
+    for i, o in [(3, 7), (5, 11)]:
+        want.append(orc.port.local_rx(red, o))
+        s, c = orc.port.dwest(red, i, o)
+        want.append(s)
+        counts.append(c)
+    for m, w in zip(got[:4], want):
+        assert np.array_equal(m, w)
+    assert np.array_equal(got[4], counts[0]) and np.array_equal(got[5], counts[1])
