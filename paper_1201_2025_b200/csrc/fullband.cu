@@ -5,7 +5,8 @@
 //
 // One CTA (256 threads) per output pixel:
 //   1. pass 1: window means (threads over bands, samples in the reference's scan order);
-//   2. pass 2: centred samples stream through shared memory in chunks; every thread
+//   2. pass 2: centred samples stream through shared memory in chunks (register
+//      kernel: raw chunks arrive two ahead by cp.async, then one centring pass); every thread
 //      owns up to 5 register-tiled 4x4 blocks of the lower triangle of the Gram
 //      matrix and accumulates them in fp64 (N L^2 MACs: the dense contraction);
 //   3. the bordered matrix [C + delta I, d; d^T, 0] is written packed (lower, row-major)
@@ -384,12 +385,20 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     for (int k = t; k < N + NI; k += blockDim.x)
         base[k] = k < N ? sample_base(P, ri, c, k, size, excl) : sample_base(P, ri, c, k - N, excl, 0);
     __syncthreads();
+    // window means: one band per thread, 8 independent partial sums (8 loads in flight;
+    // summation order differs from a sequential loop only at rounding level)
+    auto band_sum = [&](int b, int k0, int n) {
+        double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        int k = 0;
+        for (; k + 8 <= n; k += 8)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] += ld(P, base[k0 + k + u] + b);
+        for (; k < n; ++k) p[0] += ld(P, base[k0 + k] + b);
+        return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+    };
     for (int b = t; b < MP; b += blockDim.x) {
-        double sum = 0.0, si = 0.0;
-        if (b < L) {
-            for (int k = 0; k < N; ++k) sum += ld(P, base[k] + b);
-            for (int k = 0; k < NI; ++k) si += ld(P, base[N + k] + b);
-        }
+        const double sum = b < L ? band_sum(b, 0, N) : 0.0;
+        const double si = (b < L && NI > 0) ? band_sum(b, N, NI) : 0.0;
         mu[b] = b < L ? sum / N : 0.0;
         mu[MP + b] = (b < L && P.algo == HSAD_DWRX) ? si / (excl * excl) : 0.0;
     }
@@ -410,6 +419,7 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+#ifdef HSAD_FB_SYNC_CHUNKS
     for (int k0 = 0; k0 < N; k0 += CH) {
         const int nk = min(CH, N - k0);
         __syncthreads();
@@ -426,6 +436,69 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
             }
         }
         __syncthreads();
+#else
+    // Chunks of CH window samples arrive in a double-buffered raw stage by cp.async
+    // (4/8-byte LDGSTS per element, all threads, no registers held), two chunks
+    // ahead; each chunk is then centred and widened into xs by every thread in one
+    // short pass, so the global-load latency hides behind the previous chunk's Gram.
+    const int EB = P.elem_bytes;
+    unsigned char* raw = reinterpret_cast<unsigned char*>(base + size * size);  // after the offsets
+    const int raw_stride = CH * L * EB;  // bytes per stage buffer
+    const int nchunks = (N + CH - 1) / CH;
+    auto issue = [&](int j) {
+        const int k0 = j * CH, nk = min(CH, N - k0);
+        unsigned char* dstb = raw + (j & 1) * raw_stride;
+        const int total = nk * L;
+        int k = t / L, b = t % L;
+        const int dk = blockDim.x / L, db = blockDim.x % L;
+        for (int e = t; e < total; e += blockDim.x) {
+            const char* src = static_cast<const char*>(P.cube) + (base[k0 + k] + b) * EB;
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(dstb + e * EB));
+            if (EB == 8)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+            k += dk;
+            b += db;
+            if (b >= L) {
+                b -= L;
+                ++k;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // padding bands [L, MP) of xs stay zero for every chunk
+    for (int e = t; e < CH * (MP - L); e += blockDim.x) {
+        const int k = e / (MP - L), b = L + e % (MP - L);
+        xs[k * S + (b >> 3) * 10 + (b & 7)] = 0.0;
+    }
+    issue(0);
+    if (nchunks > 1) issue(1);
+    for (int j = 0; j < nchunks; ++j) {
+        const int k0 = j * CH, nk = min(CH, N - k0);
+        if (j + 1 < nchunks) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();  // chunk j landed for every thread; the Gram of chunk j-1 is done
+        {
+            const unsigned char* srcb = raw + (j & 1) * raw_stride;
+            const int total = nk * L;
+            int k = t / L, b = t % L;
+            const int dk = blockDim.x / L, db = blockDim.x % L;
+            for (int e = t; e < total; e += blockDim.x) {
+                const double v = EB == 8 ? reinterpret_cast<const double*>(srcb)[e]
+                                         : static_cast<double>(reinterpret_cast<const float*>(srcb)[e]);
+                xs[k * S + (b >> 3) * 10 + (b & 7)] = v - mu[b];
+                k += dk;
+                b += db;
+                if (b >= L) {
+                    b -= L;
+                    ++k;
+                }
+            }
+        }
+        __syncthreads();  // xs holds chunk j; its raw buffer is free
+        if (j + 2 < nchunks) issue(j + 2);
+#endif
         if (own) {
             const double* xa = xs + 10 * ti;
             const double* xb = xs + 10 * tk;
@@ -642,7 +715,8 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
         P.mp = mp8;
         P.chunk = 32;
         const size_t smem = (static_cast<size_t>(P.chunk) * (P.mp / 8) * 10 + 3 * P.mp +
-                             2 * (8 * (P.mp / 8) * 10 + 8) + nsamp) * 8;
+                             2 * (8 * (P.mp / 8) * 10 + 8) + nsamp) * 8 +
+                            2 * static_cast<size_t>(P.chunk) * P.bands * P.elem_bytes;  // cp.async stage
         HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_reg_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
