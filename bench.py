@@ -211,6 +211,22 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def detector_ncu():
+    """Issue-active and fp64-pipe utilisation of the four detector launches from the
+    committed ncu --set full capture of this workload (the detectors' own roofline is
+    fp64 issue, not HBM: ~57 B/px of DRAM traffic per launch)."""
+    f = ROOT / "profiles" / "ncu_full_r1_sweep_b.json"
+    if not f.exists():
+        return {}
+    d = json.loads(f.read_text())
+    det = [k for k in d["c5_sweep_step"] if k["launch"].startswith("detect")]
+    key_i = "smsp__issue_active.avg.pct_of_peak_sustained_active"
+    key_f = "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"
+    return {"ncu_issue_active_frac": [round(float(k[key_i]) / 100, 3) for k in det],
+            "ncu_fp64_pipe_frac": [round(float(k[key_f]) / 100, 3) for k in det],
+            "ncu_source": "profiles/ncu_full_r1_sweep_b.json (launches 7/3, 11/5, 15/5, 21/7)"}
+
+
 def workload_config(args, cfg):
     sweep = ", ".join(f"{i}/{o}" for i, o in SWEEP)
     return {"workload": f"{args.config}: {cfg['lines']}x{cfg['samples']}x{cfg['bands']} fp32 BIP, "
@@ -410,9 +426,9 @@ def run_b200(args, cfg, rank, world, local, dist):
                 "reduce (K1, HBM-bound)": {"ms": red_ms, "achieved_gbs": red_gbs,
                                            "frac": red_gbs / peak,
                                            "bytes": "fp32 cube read + fp64 reduced write"},
-                "detect (K2-K4 fused, 4 launches, fp64-compute-bound)": {"ms": det_ms,
-                                                             "share": det_ms / (red_ms + det_ms),
-                                                             "px_per_s": local_px / (det_ms / 1e3)},
+                "detect (K2-K4 fused, 4 launches, fp64-compute-bound)": dict(
+                    {"ms": det_ms, "share": det_ms / (red_ms + det_ms),
+                     "px_per_s": local_px / (det_ms / 1e3)}, **detector_ncu()),
             },
         },
         "clocks": clk,
