@@ -153,6 +153,11 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
     }
     const int64_t quantum = row_quantum(lines, samples);
     int64_t strip = (lines + kMaxStrips - 1) / kMaxStrips;
+    // a strip moves at least ~8 MB (~150 us of PCIe): smaller strips only add launch and
+    // event overhead (a 64 x 64 x 189 cube is one 3 MB strip)
+    const int64_t row_bytes = samples * bands * static_cast<int64_t>(sizeof(float));
+    const int64_t min_rows = row_bytes > 0 ? ((8 << 20) + row_bytes - 1) / row_bytes : lines;
+    if (strip < min_rows) strip = min_rows;
     strip = (strip + quantum - 1) / quantum * quantum;
     if (strip < quantum) strip = quantum;
 
