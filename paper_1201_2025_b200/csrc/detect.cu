@@ -85,6 +85,7 @@ struct DetectParams {
     ReqDev req[kMaxRequests];
     int std_layout;  // box 0 = LRX/outer window for every request, box 1 = inner box
     int staged;      // STD kernel: the update rows arrive in shared memory by TMA bulk copies
+    unsigned char* zflag;  // per-CTA "saw an all-zero spectrum" (fast pass -> counting pass)
     int has_dual;
     double n_in, n_ann;  // standard-layout dual counts
     unsigned long long* status;
@@ -99,7 +100,16 @@ struct Dim {
     static constexpr int S2 = NC2 | 1;              // odd double2 stride: conflict-free LDS.128
 };
 
+// nonzero-count table: NBOX x ncol ints, in double2 (16-byte) units
+__host__ __device__ inline int nz_pairs(int nbox, int ncol) { return (nbox * ncol * 4 + 15) / 16; }
+
+// Fast pass (ZC = false): set when the CTA has loaded an all-zero spectrum. Such a CTA's
+// tile is recomputed by the counting pass (ZC = true), so its own error reports
+// (possibly from rounding residue in all-zero windows) are suppressed.
+__shared__ int s_zero_seen;
+
 __device__ __forceinline__ void report(const DetectParams& P, int64_t row, int64_t col, int code) {
+    if (s_zero_seen) return;
     const unsigned long long packed =
         (static_cast<unsigned long long>(row * P.samples + col) << 8) |
         static_cast<unsigned long long>(code);
@@ -142,6 +152,18 @@ __device__ __forceinline__ void load_row(const DetectParams& P, const char* colb
 #pragma unroll
         for (int i = 0; i < L; ++i) y[i] = static_cast<double>(__ldg(f + i));
     }
+}
+
+// 1 if the (unshifted) spectrum has any nonzero band (-0.0 == 0.0), integer ops only
+template <int L>
+__device__ __forceinline__ int nonzero(const double (&x)[L]) {
+    uint32_t lo = 0, hi = 0;  // OR of the 32-bit halves (LOP3), sign bits dropped
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        lo |= static_cast<uint32_t>(__double2loint(x[i]));
+        hi |= static_cast<uint32_t>(__double2hiint(x[i]));
+    }
+    return ((hi & 0x7fffffffu) | lo) != 0u;
 }
 
 // m = (y, y_i y_j for i <= j), y already shifted
@@ -197,16 +219,22 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
 // mean and covariance (divisor N) from box sums: C = S2/N - mu mu^T
 // (== stats.cpp:13-29 in exact arithmetic on the shifted values). Symmetric
 // matrices are stored as their upper triangle only (c[i][j], i <= j).
+//
+// A window whose samples are all exactly zero (no-data fill) has, in the reference's
+// two-pass arithmetic, mean 0 and covariance 0 exactly; the shifted sums would leave
+// rounding residue there, so `zero` (from the per-box count of nonzero spectra)
+// selects the exact covariance 0. The callers resolve the cases where the mean's
+// residue would decide the result (all-zero background and centre, both DWRX boxes).
 template <int L>
 __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n, double (&mu)[L],
-                                         double (&c)[L][L]) {
+                                         double (&c)[L][L], bool zero) {
     const double inv = fast_rcp(n);
 #pragma unroll
     for (int i = 0; i < L; ++i) mu[i] = s[i] * inv;
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
-        for (int j = i; j < L; ++j) c[i][j] = fma(-mu[i], mu[j], s[tri<L>(i, j)] * inv);
+        for (int j = i; j < L; ++j) c[i][j] = zero ? 0.0 : fma(-mu[i], mu[j], s[tri<L>(i, j)] * inv);
 }
 
 // regularized_inverse + quadratic form (stats.cpp:31-62, detect.cpp:179-180):
@@ -492,11 +520,16 @@ __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s
 // LRX (detect.cpp:168-188) on background sums bg, count n: score = max(d^T (C+dI)^-1 d, 0)
 template <int L>
 __device__ __forceinline__ void lrx_solve(const DetectParams& P, const ReqDev& R,
-                                          const double (&bg)[Dim<L>::NC], double n_bg,
-                                          const double (&yc)[L], int64_t r, int64_t col, int64_t o,
-                                          int64_t lin) {
+                                          const double (&bg)[Dim<L>::NC], double n_bg, bool bg_zero,
+                                          int nzc, const double (&yc)[L], int64_t r, int64_t col,
+                                          int64_t o, int64_t lin) {
+    if (bg_zero) {  // C = 0, delta = 0: d = 0 -> 0 (detect.cpp:175-177), else singular
+        if (nzc) report(P, r, col, HSAD_E_SINGULAR_AFTER_RIDGE);
+        store_score(R, o, 0.0);
+        return;
+    }
     double mu[L], cm[L][L], dv[L];
-    mean_cov<L>(bg, n_bg, mu, cm);
+    mean_cov<L>(bg, n_bg, mu, cm, false);
     double dmax = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i) {
@@ -524,21 +557,23 @@ struct DualStats {
 template <int L>
 __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
                                            const double (&s_box)[Dim<L>::NC], double n_in,
-                                           double n_ann, DualStats<L>& D) {
+                                           double n_ann, bool in_zero, bool ann_zero,
+                                           DualStats<L>& D) {
     constexpr int NC = Dim<L>::NC;
     double sann[NC], mu_in[L], mu_out[L];
 #pragma unroll
     for (int c = 0; c < NC; ++c) sann[c] = s_box[c] - s_in[c];
-    mean_cov<L>(s_in, n_in, mu_in, D.cd);
-    mean_cov<L>(sann, n_ann, mu_out, D.c_out);
+    mean_cov<L>(s_in, n_in, mu_in, D.cd, in_zero);
+    mean_cov<L>(sann, n_ann, mu_out, D.c_out, ann_zero);
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
         for (int j = i; j < L; ++j) D.cd[i][j] -= D.c_out[i][j];
     D.mmax = 0.0;
+    const bool both_zero = in_zero && ann_zero;  // m_diff = 0 - 0 exactly
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-        D.md[i] = mu_in[i] - mu_out[i];
+        D.md[i] = both_zero ? 0.0 : mu_in[i] - mu_out[i];
         D.mmax = fmax(D.mmax, fabs(D.md[i]));
     }
 }
@@ -604,6 +639,15 @@ __device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>&
     if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
 }
 
+template <int NBOX>
+__device__ __forceinline__ int select_cnt(const int (&cnt)[NBOX], int k) {
+    int v = cnt[0];
+#pragma unroll
+    for (int kk = 1; kk < NBOX; ++kk)
+        if (k == kk) v = cnt[kk];
+    return v;
+}
+
 template <int L, int NBOX>
 __device__ __forceinline__ void select_box(const double (&S)[NBOX][Dim<L>::NC], int k,
                                            double (&out)[Dim<L>::NC]) {
@@ -622,10 +666,12 @@ __device__ __forceinline__ void select_box(const double (&S)[NBOX][Dim<L>::NC], 
 // shared outer/LRX window, box 1 the inner box, LRX excluding only the centre —
 // box indices are compile-time and the inner/annulus statistics are computed
 // once for DWRX and DWEST; other layouts select boxes at run time.
-template <int L, int NBOX, bool STD>
+template <int L, int NBOX, bool STD, bool ZC>
 __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev* s_req,
                                             const double (&S)[NBOX][Dim<L>::NC],
-                                            const double (&yc)[L], int64_t r, int64_t col) {
+                                            const int (&cnt)[NBOX], int nzc, const double (&yc)[L],
+                                            int64_t r, int64_t col) {
+    // cnt[k]: nonzero spectra in box k; nzc: the centre spectrum is nonzero
     constexpr int NC = Dim<L>::NC;
     const int64_t o = (r - P.row_begin) * P.samples + col;
     const int64_t lin = r * P.samples + col;
@@ -637,7 +683,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
 #pragma unroll
             for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
             add_moments<L>(bg, yc, -1.0);
-            lrx_solve<L>(P, R, bg, R.n_a, yc, r, col, o, lin);
+            lrx_solve<L>(P, R, bg, R.n_a, ZC && cnt[0] - nzc == 0, nzc, yc, r, col, o, lin);
         }
 #ifdef HSAD_PHASE_TIMERS
         long long q0 = clock64();  // phases 5/6 sampled on thread 0 of each CTA (x128)
@@ -645,7 +691,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
         if constexpr (NBOX >= 2) {
             if (P.has_dual) {
                 DualStats<L> D;
-                dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, D);
+                dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, ZC && cnt[1] == 0, ZC && cnt[0] - cnt[1] == 0, D);
                 for (int q = 0; q < P.nreq; ++q)  // DWRX first: C_ann dies before the eigensolve
                     if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L>(P, s_req[q], D, r, col, o, lin);
 #ifdef HSAD_PHASE_TIMERS
@@ -667,21 +713,26 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
             if (R.algo == HSAD_LRX) {
                 double bg[NC];
                 select_box<L, NBOX>(S, R.box_a, bg);
+                int nz_bg = select_cnt<NBOX>(cnt, R.box_a);
                 if (R.box_b < 0) {
                     add_moments<L>(bg, yc, -1.0);
+                    nz_bg -= nzc;
                 } else {
                     double g[NC];
                     select_box<L, NBOX>(S, R.box_b, g);
 #pragma unroll
                     for (int c = 0; c < NC; ++c) bg[c] -= g[c];
+                    nz_bg -= select_cnt<NBOX>(cnt, R.box_b);
                 }
-                lrx_solve<L>(P, R, bg, R.n_a, yc, r, col, o, lin);
+                lrx_solve<L>(P, R, bg, R.n_a, ZC && nz_bg == 0, nzc, yc, r, col, o, lin);
             } else {
                 double s_in[NC], s_box[NC];
                 select_box<L, NBOX>(S, R.box_b, s_in);
                 select_box<L, NBOX>(S, R.box_a, s_box);
+                const int nz_in = select_cnt<NBOX>(cnt, R.box_b);
+                const int nz_box = select_cnt<NBOX>(cnt, R.box_a);
                 DualStats<L> D;
-                dual_stats<L>(s_in, s_box, R.n_a, R.n_b, D);
+                dual_stats<L>(s_in, s_box, R.n_a, R.n_b, ZC && nz_in == 0, ZC && nz_box - nz_in == 0, D);
                 if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, R, D, r, col, o, lin);
                 else dwest_solve<L>(R, D, o);
             }
@@ -701,7 +752,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
 //   3. barrier before the next row's update.
 // Smem column stride: S2 double2 per column plus one pad pair after every K
 // columns, so the per-thread segments (stride K columns) hit distinct banks.
-template <int L, int NBOX, int K, bool STD>
+template <int L, int NBOX, int K, bool STD, bool ZC>
 // 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
 // fp64 operations, and extra warps hide their latency better than the registers
 // a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
@@ -718,7 +769,13 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
 
     const int t = threadIdx.x;
     const int NT = blockDim.x;
+    if constexpr (ZC) {  // counting pass after a fast pass: only the CTAs that met zeros
+        if (P.zflag && !P.zflag[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x]) return;
+    }
     if (t < P.nreq) s_req[t] = P.req[t];  // dynamic request index -> shared memory
+    if (t == 0) s_zero_seen = 0;
+    __syncthreads();
+
     const int ncol = P.tw + 2 * P.rmax;            // strip columns incl. halo
     // pairs per box: S2 (odd) per column + one pad pair per K columns when K > 1,
     // so a thread-to-thread stride of K*S2 + 1 pairs stays odd (conflict-free LDS.128)
@@ -746,10 +803,12 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
         const int dcol = mirror32(static_cast<int>(vcol), static_cast<int>(P.samples));
         return static_cast<const char*>(P.cube) + static_cast<int64_t>(dcol) * L * P.elem_bytes;
     };
-    auto shifted = [&](const char* cb, int64_t vrow, double (&y)[L]) {
+    auto shifted = [&](const char* cb, int64_t vrow, double (&y)[L]) -> int {
         load_row<L, STD>(P, cb, row_bytes, static_cast<int>(vrow), y);
+        const int nz = nonzero<L>(y);
 #pragma unroll
         for (int i = 0; i < L; ++i) y[i] -= shift[i];
+        return nz;
     };
 
     // STD (fp64 cube): the entering and leaving rows of every box for the update of
@@ -759,7 +818,11 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
     // memory instead of waiting on L2/HBM. stage[(2k + dir) * ncol + col][L].
     const int64_t st_lo = c0 - P.rmax > 0 ? c0 - P.rmax : 0;
     const int64_t st_hi = c0 + P.tw + P.rmax < P.samples ? c0 + P.tw + P.rmax : P.samples;
-    double* stage = reinterpret_cast<double*>(s_v2 + NBOX * box_stride);
+    // per strip column and box: count of nonzero spectra in the vertical window
+    // per strip column and box: nonzero spectra in the column's vertical window (kept
+    // like the window sums: + entering row, - leaving row)
+    int* s_nz = reinterpret_cast<int*>(s_v2 + NBOX * box_stride);  // [NBOX][ncol]
+    double* stage = reinterpret_cast<double*>(s_v2 + NBOX * box_stride + nz_pairs(NBOX, ncol));
     auto issue_rows = [&](int64_t rr) {  // thread 0 only
         const uint32_t seg = static_cast<uint32_t>((st_hi - st_lo) * L * sizeof(double));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -794,11 +857,14 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
 #pragma unroll
             for (int i = 0; i < NC; ++i) v[i] = 0.0;
             const int R = P.radius[k];
+            int nzc = 0;
             for (int d = -R; d <= R; ++d) {
                 double y[L];
-                shifted(cb, ra + d, y);
+                nzc += shifted(cb, ra + d, y);
                 add_moments<L>(v, y, 1.0);
             }
+            if constexpr (ZC) s_nz[k * ncol + c] = nzc;
+            else if (k == 0 && nzc != 2 * R + 1) s_zero_seen = 1;
             double2* dst = vslot(k, c);
 #pragma unroll
             for (int c2 = 0; c2 < NC2; ++c2)
@@ -814,7 +880,8 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
         // K = 1: fetch the centre spectrum first; its latency hides behind the
         // vertical update, the barrier and the horizontal sums
         double yc1[L];
-        if (owner1) shifted(own_cb, r, yc1);
+        int nzc1 = 0;
+        if (owner1) nzc1 = shifted(own_cb, r, yc1);
         if (r > ra) {
             if constexpr (STD) {
                 mbar_wait(&s_bar, st_phase);
@@ -834,6 +901,7 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
                 for (int k = 0; k < NBOX; ++k) {
                     const int R = P.radius[k];
                     double yin[L], yout[L], dm[NC];
+                    int nz_in, nz_out;
                     if constexpr (STD) {
                         const double* si = stage + (static_cast<int64_t>(2 * k) * ncol + scol) * L;
                         const double* so = si + static_cast<int64_t>(ncol) * L;
@@ -841,15 +909,27 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
                         for (int i = 0; i < L; i += 2) {
                             const double2 a = *reinterpret_cast<const double2*>(si + i);
                             const double2 b = *reinterpret_cast<const double2*>(so + i);
-                            yin[i] = a.x - shift[i];
-                            yin[i + 1] = a.y - shift[i + 1];
-                            yout[i] = b.x - shift[i];
-                            yout[i + 1] = b.y - shift[i + 1];
+                            yin[i] = a.x;
+                            yin[i + 1] = a.y;
+                            yout[i] = b.x;
+                            yout[i + 1] = b.y;
+                        }
+                        nz_in = nonzero<L>(yin);
+                        nz_out = nonzero<L>(yout);
+#pragma unroll
+                        for (int i = 0; i < L; ++i) {
+                            yin[i] -= shift[i];
+                            yout[i] -= shift[i];
                         }
                     } else {
-                        shifted(cb, r + R, yin);
-                        shifted(cb, r - 1 - R, yout);
+                        nz_in = shifted(cb, r + R, yin);
+                        nz_out = shifted(cb, r - 1 - R, yout);
                     }
+                    // fast pass: every spectrum of any window enters box 0 (the widest, in
+                    // the standard layout) or sits in its initial window, so checking box 0's
+                    // entering rows finds every zero spectrum
+                    if constexpr (ZC) s_nz[k * ncol + c] += nz_in - nz_out;
+                    else if (k == 0 && !nz_in) s_zero_seen = 1;
 #pragma unroll
                     for (int i = 0; i < NC; ++i) dm[i] = 0.0;
                     add_moments<L>(dm, yin, 1.0);
@@ -873,13 +953,16 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
         PT_MARK(1);  // barrier A
         if (seg0 < P.tw && c0 + seg0 < P.samples) {
             double S[NBOX][NC];
+            int cnt[NBOX];
             // horizontal window of the first column of the segment
 #pragma unroll
             for (int k = 0; k < NBOX; ++k) {
 #pragma unroll
                 for (int i = 0; i < NC; ++i) S[k][i] = 0.0;
                 const int R = P.radius[k];
+                int ck = 0;
                 for (int d = -R; d <= R; ++d) {
+                    if constexpr (ZC) ck += s_nz[k * ncol + P.rmax + seg0 + d];
                     const double2* src = vslot(k, P.rmax + seg0 + d);
 #pragma unroll
                     for (int c2 = 0; c2 < NC2; ++c2) {
@@ -888,6 +971,7 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
                         if (2 * c2 + 1 < NC) S[k][2 * c2 + 1] += v.y;
                     }
                 }
+                cnt[k] = ck;
             }
 #pragma unroll 1
             for (int j = 0; j < K; ++j) {
@@ -898,6 +982,8 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
 #pragma unroll
                     for (int k = 0; k < NBOX; ++k) {
                         const int R = P.radius[k];
+                        if constexpr (ZC)
+                            cnt[k] += s_nz[k * ncol + P.rmax + sc + R] - s_nz[k * ncol + P.rmax + sc - 1 - R];
                         const double2* in = vslot(k, P.rmax + sc + R);
                         const double2* out = vslot(k, P.rmax + sc - 1 - R);
 #pragma unroll
@@ -909,19 +995,25 @@ __global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kern
                     }
                 }
                 double yc[L];
+                int nzc;
                 if (K == 1) {
 #pragma unroll
                     for (int i = 0; i < L; ++i) yc[i] = yc1[i];
+                    nzc = nzc1;
                 } else {
-                    shifted(colbase_of(P.rmax + sc), r, yc);
+                    nzc = shifted(colbase_of(P.rmax + sc), r, yc);
                 }
                 PT_MARK(2);  // horizontal + centre load
-                solve_pixel<L, NBOX, STD>(P, s_req, S, yc, r, col);
+                solve_pixel<L, NBOX, STD, ZC>(P, s_req, S, cnt, nzc, yc, r, col);
                 PT_MARK(3);  // solves
             }
         }
         __syncthreads();
         PT_MARK(4);  // barrier B
+    }
+    if constexpr (!ZC) {
+        if (t == 0 && s_zero_seen && P.zflag)
+            P.zflag[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = 1;
     }
     PT_FLUSH();
 }
@@ -934,15 +1026,21 @@ size_t stage_bytes(int nbox, int64_t ncol, int bands) {
 template <int L, int NB>
 cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
     const int ncol = P.tw + 2 * P.rmax;
-    auto go = [&](auto kern, int K, bool staged) -> cudaError_t {
-        const size_t smem = static_cast<size_t>(NB) *
-                                (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)) * sizeof(double2) +
+    auto go = [&](auto kern, int K, bool staged, bool two_pass) -> cudaError_t {
+        const size_t smem = (static_cast<size_t>(NB) * (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)) +
+                             nz_pairs(NB, ncol)) * sizeof(double2) +
                             (staged ? stage_bytes(NB, ncol, L) : 0);
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        kern<<<grid, nt, smem, s>>>(P);
+        if (two_pass) {
+            kern<<<grid, nt, smem, s>>>(P);
+        } else {
+            DetectParams Q = P;
+            Q.zflag = nullptr;  // single counting pass over every CTA
+            kern<<<grid, nt, smem, s>>>(Q);
+        }
         return cudaGetLastError();
     };
     if constexpr (L == 4) {  // multi-column segments only on the 4-band (DWT) hot path
@@ -950,16 +1048,20 @@ cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaS
         // kernel without the general box-selection path and the fp32 load path
         // (smaller code: fewer instruction-cache misses, measured -5% on C5)
         if constexpr (NB <= 2) {
-            if (P.staged) {
-                if (kcols == 4) return go(detect_kernel<L, NB, 4, true>, 4, true);
-                if (kcols == 2) return go(detect_kernel<L, NB, 2, true>, 2, true);
-                if (kcols == 1) return go(detect_kernel<L, NB, 1, true>, 1, true);
+            if (P.staged) {  // fast pass, then the counting pass over CTAs that met zeros
+                auto both = [&](auto fast, auto counting, int K) -> cudaError_t {
+                    cudaError_t e = go(fast, K, true, true);
+                    return e != cudaSuccess ? e : go(counting, K, true, true);
+                };
+                if (kcols == 4) return both(detect_kernel<L, NB, 4, true, false>, detect_kernel<L, NB, 4, true, true>, 4);
+                if (kcols == 2) return both(detect_kernel<L, NB, 2, true, false>, detect_kernel<L, NB, 2, true, true>, 2);
+                if (kcols == 1) return both(detect_kernel<L, NB, 1, true, false>, detect_kernel<L, NB, 1, true, true>, 1);
             }
         }
-        if (kcols == 4) return go(detect_kernel<L, NB, 4, false>, 4, false);
-        if (kcols == 2) return go(detect_kernel<L, NB, 2, false>, 2, false);
+        if (kcols == 4) return go(detect_kernel<L, NB, 4, false, true>, 4, false, false);
+        if (kcols == 2) return go(detect_kernel<L, NB, 2, false, true>, 2, false, false);
     }
-    if (kcols == 1) return go(detect_kernel<L, NB, 1, false>, 1, false);
+    if (kcols == 1) return go(detect_kernel<L, NB, 1, false, true>, 1, false, false);
     return cudaErrorInvalidValue;
 }
 
@@ -974,8 +1076,8 @@ cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, int kcols, cudaSt
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_detect(int bands, const DetectParams& P, dim3 grid, int nt, int kcols,
-                          cudaStream_t s) {
+cudaError_t launch_bands(int bands, const DetectParams& P, dim3 grid, int nt, int kcols,
+                         cudaStream_t s) {
     switch (bands) {
         case 1: return launch_l<1>(P, grid, nt, kcols, s);
         case 2: return launch_l<2>(P, grid, nt, kcols, s);
@@ -987,6 +1089,43 @@ cudaError_t launch_detect(int bands, const DetectParams& P, dim3 grid, int nt, i
         case 8: return launch_l<8>(P, grid, nt, kcols, s);
     }
     return cudaErrorInvalidValue;
+}
+
+// Stream-ordered scratch (flags, status words) comes from the device's default memory
+// pool; with the default release threshold (0) the pool returns its memory at every
+// synchronisation and the next cudaMallocAsync maps pages again (measured: ~10 ms
+// stalls). Keep the pool's memory once per process and device.
+void keep_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
+
+// The staged (standard-layout fp64) kernel runs as a fast pass plus a counting pass
+// that recomputes only the CTAs which met an all-zero spectrum; their per-CTA flags
+// live in a stream-ordered scratch allocation.
+cudaError_t launch_detect(int bands, const DetectParams& P0, dim3 grid, int nt, int kcols,
+                          cudaStream_t s) {
+    DetectParams P = P0;
+    P.zflag = nullptr;
+    unsigned char* flags = nullptr;
+    if (P.staged) {
+        keep_pool_memory();
+        const size_t n = static_cast<size_t>(grid.x) * grid.y;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flags), n, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, n, s);
+        if (e != cudaSuccess) return e;
+        P.zflag = flags;
+    }
+    const cudaError_t e = launch_bands(bands, P, grid, nt, kcols, s);
+    if (flags) cudaFreeAsync(flags, s);
+    return e;
 }
 
 const char* algo_name(int a) {
@@ -1109,7 +1248,7 @@ int64_t row_quantum(int64_t lines, int64_t samples) {
     const int64_t strips = (samples + tw - 1) / tw;
     // 32 measured best on C5 (24..128 sweep: within 1% of 24, 3.6% faster than 64)
     int64_t q = 32;
-    while (q > 8 && strips * ((lines + q - 1) / q) < 2 * sms) q /= 2;
+    while (q > 2 && strips * ((lines + q - 1) / q) < 2 * sms) q /= 2;
     return q;
 }
 
@@ -1187,7 +1326,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     auto smem_for = [&](int k) {
         const int64_t ncol = 128 * k + 2 * P.rmax;
         const int s2 = ((bands + bands * (bands + 1) / 2 + 1) / 2) | 1;
-        return static_cast<int64_t>(P.nbox) * (ncol * s2 + (k > 1 ? ncol / k + 1 : 0)) * 16;
+        return (static_cast<int64_t>(P.nbox) * (ncol * s2 + (k > 1 ? ncol / k + 1 : 0)) +
+                nz_pairs(P.nbox, static_cast<int>(ncol))) * 16;
     };
     // <= 56 KB keeps 4 CTAs per SM (228 KB shared memory); K shrinks to fit
     const int64_t smem_cap = getenv("HSAD_SMEM_CAP_KB") ? atoi(getenv("HSAD_SMEM_CAP_KB")) * 1024 : 56 * 1024;

@@ -82,7 +82,7 @@ def test_strip_rows_and_quantum():
     assert lib.hsad_strip_rows(100, 0, 10, req, 1, C.byref(r0), C.byref(n)) == 0
     assert (r0.value, n.value) == (0, 15)  # rows -5..-1 reflect onto 1..5
     q = lib.hsad_row_quantum(4096, 4096)
-    assert q in (8, 16, 32, 64)
+    assert q in (2, 4, 8, 16, 32, 64)
 
 
 def test_decode_status():

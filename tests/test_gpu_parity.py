@@ -543,11 +543,19 @@ def test_pipeline_host_error_matches_device_path(orc, lines):
         cube = np.zeros((5, 5, 64), dtype=np.float32)
         cube[2, 2] = 1.0
     else:
+        # a no-data (all-zero) block with one lit pixel: its background / annulus is
+        # exactly zero, so the reference fails there (C = 0, delta = 0, d != 0)
         cube = orc.port.random_cube(lines, 40, 64, 12).astype(np.float32)
         cube[300:320] = 0.0
+        cube[310, 20] = 1.0
     reqs = [hs.DetectRequest("lrx", W1(3)), hs.DetectRequest("dwrx", W2(1, 3))]
+    red_o = orc.port.reduce_cube(cube.astype(np.float64), 2, 4)
+    with pytest.raises(OracleError) as ref_err:
+        orc.port.local_rx(red_o, 3)
     with pytest.raises(hs.HsadError) as want:
         hs.reduce_detect(gpu(cube), reqs)
+    assert (want.value.name, want.value.row, want.value.col) == (ref_err.value.name, ref_err.value.row,
+                                                                 ref_err.value.col)
     outs = [(torch.empty((lines, cube.shape[1]), dtype=torch.float64), None) for _ in reqs]
     with pytest.raises(hs.HsadError) as got:
         hs.pipeline_host(torch.as_tensor(cube), 2, 4, reqs, outs)
@@ -646,3 +654,22 @@ def test_staged_kernel_multi_column(orc, monkeypatch, lines, samples):
     plain = run(cube, reqs)
     assert np.array_equal(staged[0][0], plain[0][0])
     assert max_rel_diff(staged[0][0], orc.port.local_rx(cube, 11)) < TOL64
+
+
+def test_zero_block_matches_reference_exactly(orc):
+    """No-data fill: windows whose samples are all exactly zero have mean 0 and
+    covariance 0 in the reference (two-pass); the kernel's shifted sums must not leave
+    rounding residue there (scores exactly 0 inside the block, oracle parity around it)."""
+    cube = orc.port.random_cube(90, 70, 4, 33)
+    cube[30:55, 10:40] = 0.0
+    cube[:, 60:] = 0.0  # a zero border strip
+    reqs = [hs.DetectRequest("lrx", W1(5)), hs.DetectRequest("dwrx", W2(3, 7)),
+            hs.DetectRequest("dwest", W2(3, 7), eigcount=True)]
+    for shape_cube in (cube, cube[:, :, :3].copy()):
+        (l, _), (d, _), (e, n) = run(shape_cube, reqs)
+        assert max_rel_diff(l, orc.port.local_rx(shape_cube, 5)) < TOL64
+        assert max_rel_diff(d, orc.port.dwrx(shape_cube, 3, 7)) < TOL64
+        s_, c_ = orc.port.dwest(shape_cube, 3, 7)
+        assert max_rel_diff(e, s_) < TOL64 and np.array_equal(n, c_)
+        assert np.all(l[35:50, 15:35] == 0.0) and np.all(d[35:50, 15:35] == 0.0)
+        assert np.all(e[35:50, 15:35] == 0.0) and np.all(l[:, 64:] == 0.0)
