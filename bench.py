@@ -215,16 +215,18 @@ def detector_ncu():
     """Issue-active and fp64-pipe utilisation of the four detector launches from the
     committed ncu --set full capture of this workload (the detectors' own roofline is
     fp64 issue, not HBM: ~57 B/px of DRAM traffic per launch)."""
-    f = ROOT / "profiles" / "ncu_full_r1_sweep_b.json"
+    f = ROOT / "profiles" / "ncu_full_r1_sweep_c.json"
     if not f.exists():
         return {}
     d = json.loads(f.read_text())
-    det = [k for k in d["c5_sweep_step"] if k["launch"].startswith("detect")]
+    order = ["detect 3/7", "detect 5/11", "detect 5/15", "detect 7/21"]
+    det = sorted((k for k in d["c5_sweep_step"] if k["launch"] in order),
+                 key=lambda k: order.index(k["launch"]))
     key_i = "smsp__issue_active.avg.pct_of_peak_sustained_active"
     key_f = "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"
     return {"ncu_issue_active_frac": [round(float(k[key_i]) / 100, 3) for k in det],
             "ncu_fp64_pipe_frac": [round(float(k[key_f]) / 100, 3) for k in det],
-            "ncu_source": "profiles/ncu_full_r1_sweep_b.json (launches 7/3, 11/5, 15/5, 21/7)"}
+            "ncu_source": "profiles/ncu_full_r1_sweep_c.json (fast passes of the 7/3, 11/5, 15/5, 21/7 detectors)"}
 
 
 def workload_config(args, cfg):
@@ -404,7 +406,7 @@ def run_b200(args, cfg, rank, world, local, dist):
     step_gbs = value * 1e6 * bpp / 1e9
     # DRAM traffic per launch from the committed ncu --set full capture of this workload
     traffic, traffic_src = None, None
-    tfile = ROOT / "profiles" / "ncu_traffic_r1_sweep_b.json"
+    tfile = ROOT / "profiles" / "ncu_traffic_r1_sweep_c.json"
     if args.config == "C5" and world == 1 and tfile.exists():
         tj = json.loads(tfile.read_text())
         traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in tj["launches"]) / 1e9

@@ -21,19 +21,33 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"]
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 LABELS = ["reduce (K1)", "detect 3/7", "detect 5/11", "detect 5/15", "detect 7/21"]
+WINDOWS = ["3/7", "5/11", "5/15", "7/21"]
+
+
+def label(i, name, seen):
+    """reduce, then the detector launches in order; a '..., 1, 1>' detect kernel is the
+    zero-window counting pass that follows each fast pass."""
+    if "reduce" in name:
+        return "reduce (K1)"
+    if name.replace(" ", "").split("(")[0].endswith(",1,1>"):
+        return f"detect {WINDOWS[(seen['fast'] - 1) % 4]} counting pass"
+    seen["fast"] += 1
+    return f"detect {WINDOWS[(seen['fast'] - 1) % 4]}"
 
 
 def main():
     rep, tag, note = sys.argv[1], sys.argv[2], sys.argv[3]
+    first = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # window index of the first detect launch
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     full, traffic = [], []
+    seen = {"fast": first}
     for i, r in enumerate(rows[2:]):
         d = dict(zip(hdr, r))
         u = dict(zip(hdr, units))
-        ent = {"kernel": d["Kernel Name"], "launch": LABELS[i] if i < len(LABELS) else f"launch {i}"}
+        ent = {"kernel": d["Kernel Name"], "launch": label(i, d["Kernel Name"], seen)}
         for m in METRICS:
             ent[m] = d.get(m)
             ent[m + "_unit"] = u.get(m)
