@@ -673,3 +673,18 @@ def test_zero_block_matches_reference_exactly(orc):
         assert max_rel_diff(e, s_) < TOL64 and np.array_equal(n, c_)
         assert np.all(l[35:50, 15:35] == 0.0) and np.all(d[35:50, 15:35] == 0.0)
         assert np.all(e[35:50, 15:35] == 0.0) and np.all(l[:, 64:] == 0.0)
+
+
+def test_maximum_window_and_limits(orc):
+    """The largest window this build supports (hsad_get_limits().max_window) on a small
+    image (many folds of the reflection), and one step past it -> Unsupported."""
+    lim = hs._abi.Limits()
+    hs._abi.lib().hsad_get_limits(lim)
+    w = lim.max_window
+    cube = orc.port.random_cube(12, 17, 4, 4242)
+    (l, _), (d, _) = run(cube, [hs.DetectRequest("lrx", W1(w)), hs.DetectRequest("dwrx", W2(w - 2, w))])
+    assert_kappa_close(l, orc.port.local_rx(cube, w), window_kappa(cube, w, 1, 1e-6), f"lrx {w}")
+    assert_kappa_close(d, orc.port.dwrx(cube, w - 2, w), window_kappa(cube, w, w - 2, 1e-6), f"dwrx {w}")
+    with pytest.raises(hs.HsadError) as e:
+        run(cube, [hs.DetectRequest("lrx", W1(w + 2))])
+    assert e.value.name == "Unsupported"
