@@ -388,6 +388,40 @@ __device__ __forceinline__ void sweep32(float (&a)[L][L], float (&v)[L][L]) {
     }
 }
 
+// L = 4 fp32 sweep with the eigenvector matrix held as packed column halves
+// vv[j][h] = (V[2h][j], V[2h+1][j]): each column rotation is four FFMA2/FMUL2 pairs
+// instead of eight scalar multiply-adds (Blackwell fp32x2).
+__device__ __forceinline__ void sweep32_4(float (&a)[4][4], float2 (&vv)[4][2]) {
+    constexpr SweepOrder<4> ord;
+#pragma unroll
+    for (int i = 0; i < SweepOrder<4>::N; ++i) {
+        const int p = ord.p[i], q = ord.q[i];
+        const float t = jacobi_t32(a[p][p], a[q][q], a[p][q]);
+        const float c = rsqrtf(fmaf(t, t, 1.0f));
+        const float s = t * c;
+        const float apq = a[p][q];
+        a[p][p] -= t * apq;
+        a[q][q] += t * apq;
+        a[p][q] = 0.0f;
+        const float2 c2 = make_float2(c, c), s2 = make_float2(s, s), ns2 = make_float2(-s, -s);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k == p || k == q) continue;
+            float& akp = sym<4, float>(a, k, p);
+            float& akq = sym<4, float>(a, k, q);
+            const float x = akp, y = akq;
+            akp = c * x - s * y;
+            akq = s * x + c * y;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 vp = vv[p][h], vq = vv[q][h];
+            vv[p][h] = __ffma2_rn(c2, vp, __fmul2_rn(ns2, vq));
+            vv[q][h] = __ffma2_rn(s2, vp, __fmul2_rn(c2, vq));
+        }
+    }
+}
+
 // fp64 polish sweep on a nearly diagonal matrix. When every lane of the warp
 // has |a_pq| < 1e-4 |a_qq - a_pp| the angle comes from the series
 // t = x (1 - x^2), x = a_pq / (a_qq - a_pp), and c = 1 - t^2/2 (both exact to
@@ -442,8 +476,26 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
 #ifndef HSAD_F32_SWEEPS
 #define HSAD_F32_SWEEPS 3
 #endif
+    if constexpr (L == 4) {  // measured -1.8% on the C5 sweep vs the scalar rotation
+        float2 vv[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            vv[j][0] = make_float2(j == 0 ? 1.0f : 0.0f, j == 1 ? 1.0f : 0.0f);
+            vv[j][1] = make_float2(j == 2 ? 1.0f : 0.0f, j == 3 ? 1.0f : 0.0f);
+        }
 #pragma unroll 1
-    for (int sweep = 0; sweep < (L <= 4 ? HSAD_F32_SWEEPS : 6); ++sweep) sweep32<L>(a32, v32);
+        for (int sweep = 0; sweep < HSAD_F32_SWEEPS; ++sweep) sweep32_4(a32, vv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v32[0][j] = vv[j][0].x;
+            v32[1][j] = vv[j][0].y;
+            v32[2][j] = vv[j][1].x;
+            v32[3][j] = vv[j][1].y;
+        }
+    } else {
+#pragma unroll 1
+        for (int sweep = 0; sweep < (L <= 4 ? HSAD_F32_SWEEPS : 6); ++sweep) sweep32<L>(a32, v32);
+    }
     // modified Gram-Schmidt in fp64
 #pragma unroll
     for (int j = 0; j < L; ++j) {
