@@ -224,8 +224,17 @@ def detector_ncu():
                  key=lambda k: order.index(k["launch"]))
     key_i = "smsp__issue_active.avg.pct_of_peak_sustained_active"
     key_f = "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"
+    def fp64_tflops(k):  # executed fp64 flops (2 per DFMA) per elapsed cycle x SM clock
+        m = "smsp__sass_thread_inst_executed_op_{}_pred_on.sum.per_cycle_elapsed"
+        try:
+            f = 2 * float(k[m.format("dfma")]) + float(k[m.format("dadd")]) + float(k[m.format("dmul")])
+        except (KeyError, TypeError, ValueError):
+            return None
+        return round(f * 1.965e9 / 1e12, 2)
     return {"ncu_issue_active_frac": [round(float(k[key_i]) / 100, 3) for k in det],
             "ncu_fp64_pipe_frac": [round(float(k[key_f]) / 100, 3) for k in det],
+            "ncu_fp64_tflops_executed": [fp64_tflops(k) for k in det],
+            "fp64_peak_tflops_measured": 35.4,
             "ncu_source": "profiles/ncu_full_r1_sweep_c.json (fast passes of the 7/3, 11/5, 15/5, 21/7 detectors)"}
 
 

@@ -18,7 +18,10 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
            "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
-           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"]
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+           "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
+           "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
+           "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed"]
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 LABELS = ["reduce (K1)", "detect 3/7", "detect 5/11", "detect 5/15", "detect 7/21"]
 WINDOWS = ["3/7", "5/11", "5/15", "7/21"]
