@@ -242,6 +242,17 @@ typedef struct hsad_cube_header { /* hsad::CubeHeader, cube.hpp:26-37 */
 hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
                            void* d_out, int32_t out_bytes, void* stream);
 
+/* read_cube followed by reduce_cube (wavelet.cpp:148-167) without the BIP intermediate:
+ * a BSQ / BIL raw cube is decoded and reduced in one pass (composed wavelet map applied
+ * per band plane row segment); BIP raw input goes through hsad_read_cube + hsad_reduce.
+ * Header / size errors as hsad_read_cube, then the wavelet parameter errors of
+ * hsad_reduce, then NonFiniteValue for the first non-finite element. d_out: BIP
+ * (lines x samples x target_bands), out_bytes 8 or 4. target_bands 1..16 (powers of 2).
+ * Synchronous. */
+hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                            int32_t order, int32_t target_bands, void* d_out, int32_t out_bytes,
+                            void* stream);
+
 /* ---- evaluation on device ------------------------------------ */
 typedef struct hsad_roc_summary {
     uint64_t positives, negatives;

@@ -78,6 +78,9 @@ hsad_status wavelet_plan(int32_t bands, int32_t order, int32_t target, std::vect
 
 hsad_status window_validate(const hsad_window& w);
 
+// Device copy of the composed target x bands wavelet map (cached per thread), reduce.cu.
+hsad_status device_wavelet_map(int32_t bands, int32_t order, int32_t target, const double** d_map);
+
 // Full-band (bands > 8) LRX / DWRX request, fullband.cu.
 struct FbParams {
     const void* cube;

@@ -226,6 +226,113 @@ cudaError_t dispatch_code(const hsad_cube_header& h, const void* raw, bool swap,
     return cudaErrorInvalidValue;
 }
 
+// ---- fused decode + DWT straight from a raw BSQ / BIL file (read_cube then reduce_cube)
+// One CTA = 128 consecutive columns of one batch (BSQ: the whole plane, BIL: one line);
+// 4 band groups of 64 threads stream their bands (each thread 2 columns 64 apart: warp
+// loads are 32 consecutive columns of one band, coalesced in BSQ/BIL; 16 loads in flight
+// per thread), apply the composed target x bands map (shared memory) and combine their
+// partial sums in a fixed order into one contiguous BIP run. The BIP fp32/fp64
+// intermediate of read_cube is never written.
+constexpr int kRawThreads = 64;  // columns per group; each thread owns kRawPPT columns
+constexpr int kRawPPT = 2;
+constexpr int kRawPix = kRawThreads * kRawPPT;  // columns per CTA
+constexpr int kRawGroups = 4;                   // band groups per CTA
+template <int CODE, int TARGET>
+__global__ void __launch_bounds__(kRawThreads * kRawGroups)
+    reduce_raw_kernel(const typename Src<CODE>::T* __restrict__ in, bool swap, int R, int64_t C,
+                      const double* __restrict__ wmap, void* __restrict__ out, int out_bytes,
+                      unsigned long long* status) {
+    using T = typename Src<CODE>::T;
+    extern __shared__ double s_dyn[];
+    double* s_w = s_dyn;                                          // [TARGET][R]
+    double* s_part = s_dyn + TARGET * R;                          // [groups][kRawPix][TARGET]
+    for (int i = threadIdx.x; i < TARGET * R; i += blockDim.x) s_w[i] = wmap[i];
+    __syncthreads();
+    const int tx = threadIdx.x % kRawThreads, g = threadIdx.x / kRawThreads;
+    const int64_t batch = blockIdx.y;
+    const int64_t cbase = static_cast<int64_t>(blockIdx.x) * kRawPix;
+    const T* src = in + batch * R * C + cbase;
+    bool live[kRawPPT];
+#pragma unroll
+    for (int m = 0; m < kRawPPT; ++m) live[m] = cbase + tx + m * kRawThreads < C;
+    double acc[kRawPPT][TARGET];
+#pragma unroll
+    for (int m = 0; m < kRawPPT; ++m)
+#pragma unroll
+        for (int j = 0; j < TARGET; ++j) acc[m][j] = 0.0;
+    constexpr int U = 8;  // band rows in flight per thread (x kRawPPT columns)
+    for (int b0 = g; b0 < R; b0 += kRawGroups * U) {
+        T raw[U][kRawPPT];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < kRawPPT; ++m) {
+                const int b = b0 + u * kRawGroups;
+                raw[u][m] = (live[m] && b < R)
+                                ? __ldg(src + static_cast<int64_t>(b) * C + tx + m * kRawThreads)
+                                : T(0);
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int b = b0 + u * kRawGroups;
+            if (b < R) {
+#pragma unroll
+                for (int m = 0; m < kRawPPT; ++m) {
+                    if (!live[m]) continue;
+                    const double v = decode<CODE>(raw[u][m], swap);
+                    check_finite<CODE>(v, (batch * C + cbase + tx + m * kRawThreads) * R + b, status);
+#pragma unroll
+                    for (int j = 0; j < TARGET; ++j) acc[m][j] = fma(s_w[j * R + b], v, acc[m][j]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < kRawPPT; ++m)
+#pragma unroll
+        for (int j = 0; j < TARGET; ++j)
+            s_part[(g * kRawPix + tx + m * kRawThreads) * TARGET + j] = acc[m][j];
+    __syncthreads();
+    // combine the band groups in a fixed order; the CTA's output run is contiguous
+    const int64_t o0 = (batch * C + cbase) * TARGET;
+    const int64_t ncols = C - cbase < kRawPix ? C - cbase : kRawPix;
+    for (int i = threadIdx.x; i < ncols * TARGET; i += blockDim.x) {
+        const double v = (s_part[i] + s_part[kRawPix * TARGET + i]) +
+                         (s_part[2 * kRawPix * TARGET + i] + s_part[3 * kRawPix * TARGET + i]);
+        if (out_bytes == 8) static_cast<double*>(out)[o0 + i] = v;
+        else static_cast<float*>(out)[o0 + i] = static_cast<float>(v);
+    }
+}
+
+template <int CODE>
+cudaError_t launch_reduce_raw(const hsad_cube_header& h, const void* raw, bool swap, int target,
+                              const double* wmap, void* out, int out_bytes,
+                              unsigned long long* status, cudaStream_t s) {
+    const int64_t plane = static_cast<int64_t>(h.lines) * h.samples;
+    const int64_t batches = h.interleave == HSAD_BSQ ? 1 : h.lines;
+    const int64_t C = h.interleave == HSAD_BSQ ? plane : h.samples;
+    if (batches > 65535) return cudaErrorInvalidConfiguration;
+    const dim3 grid(static_cast<unsigned>((C + kRawPix - 1) / kRawPix), static_cast<unsigned>(batches));
+    const size_t smem = (static_cast<size_t>(target) * h.bands +
+                         static_cast<size_t>(kRawGroups) * kRawPix * target) * sizeof(double);
+    const auto* in = static_cast<const typename Src<CODE>::T*>(raw);
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kRawThreads * kRawGroups, smem, s>>>(in, swap, h.bands, C, wmap, out, out_bytes, status);
+        return cudaGetLastError();
+    };
+    switch (target) {
+        case 1: return go(reduce_raw_kernel<CODE, 1>);
+        case 2: return go(reduce_raw_kernel<CODE, 2>);
+        case 4: return go(reduce_raw_kernel<CODE, 4>);
+        case 8: return go(reduce_raw_kernel<CODE, 8>);
+        case 16: return go(reduce_raw_kernel<CODE, 16>);
+    }
+    return cudaErrorInvalidValue;
+}
+
 int64_t element_size(int code) {  // cube.cpp:22-33
     switch (code) {
         case 1: return 1;
@@ -242,11 +349,9 @@ int64_t element_size(int code) {  // cube.cpp:22-33
 
 using namespace hsad_b200;
 
-extern "C" hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
-                                      void* d_out, int32_t out_bytes, void* stream) {
-    if (!header) return set_error(HSAD_E_INVALID_VALUE, "null header");
-    const hsad_cube_header& h = *header;
-    // CubeHeader::validate (cube.cpp:39-45), same order and messages
+namespace {
+// CubeHeader::validate + the byte count (cube.cpp:22-45, 200-203), same order and messages
+hsad_status validate_raw(const hsad_cube_header& h, int64_t raw_bytes) {
     if (h.samples < 1 || h.lines < 1 || h.bands < 1)
         return set_error(HSAD_E_INVALID_VALUE, "samples, lines and bands must all be >= 1");
     const int64_t esize = element_size(h.data_type_code);
@@ -258,9 +363,78 @@ extern "C" hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, cons
     if (h.interleave != HSAD_BSQ && h.interleave != HSAD_BIL && h.interleave != HSAD_BIP)
         return set_error(HSAD_E_INVALID_VALUE, "unknown interleave " + std::to_string(h.interleave));
     const int64_t expected = static_cast<int64_t>(h.samples) * h.lines * h.bands * esize;
-    if (raw_bytes != expected)  // cube.cpp:200-203
+    if (raw_bytes != expected)
         return set_error(HSAD_E_SIZE_MISMATCH, "raw data is " + std::to_string(raw_bytes) +
                                                    " bytes, header expects " + std::to_string(expected));
+    return HSAD_OK;
+}
+
+hsad_status nonfinite_error(const hsad_cube_header& h, unsigned long long first) {
+    const int64_t band = static_cast<int64_t>(first % h.bands);
+    const int64_t pix = static_cast<int64_t>(first / h.bands);
+    return set_error(HSAD_E_NON_FINITE_VALUE, "at (row=" + std::to_string(pix / h.samples) +
+                                                  ", col=" + std::to_string(pix % h.samples) +
+                                                  ", band=" + std::to_string(band) + ")");
+}
+}  // namespace
+
+extern "C" hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                                       int32_t order, int32_t target_bands, void* d_out,
+                                       int32_t out_bytes, void* stream) {
+    if (!header) return set_error(HSAD_E_INVALID_VALUE, "null header");
+    const hsad_cube_header& h = *header;
+    hsad_status st = validate_raw(h, raw_bytes);
+    if (st != HSAD_OK) return st;
+    if (out_bytes != 8 && out_bytes != 4)
+        return set_error(HSAD_E_INVALID_VALUE, "out_bytes must be 8 (fp64) or 4 (fp32)");
+    st = wavelet_plan(h.bands, order, target_bands, nullptr);
+    if (st != HSAD_OK) return st;
+    if (!d_raw || !d_out) return set_error(HSAD_E_INVALID_VALUE, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (h.interleave == HSAD_BIP) {
+        // BIP: decode (read_cube) into a stream-ordered fp64 cube, then the TMA DWT
+        void* tmp = nullptr;
+        const size_t n = static_cast<size_t>(h.lines) * h.samples * h.bands;
+        HSAD_CUDA_TRY(cudaMallocAsync(&tmp, n * sizeof(double), s));
+        st = hsad_read_cube(d_raw, raw_bytes, &h, tmp, 8, stream);
+        if (st == HSAD_OK)
+            st = hsad_reduce(tmp, 8, h.lines, h.samples, h.bands, order, target_bands, d_out, out_bytes, stream);
+        cudaFreeAsync(tmp, s);
+        return st;
+    }
+    if (target_bands != 1 && target_bands != 2 && target_bands != 4 && target_bands != 8 &&
+        target_bands != 16)
+        return set_error(HSAD_E_UNSUPPORTED, "raw-cube reduction supports 1..16 target bands");
+    const double* d_map = nullptr;
+    st = device_wavelet_map(h.bands, order, target_bands, &d_map);
+    if (st != HSAD_OK) return st;
+    const bool swap = h.byte_order == 1;
+    unsigned long long* status = nullptr;
+    HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
+    HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (h.data_type_code) {
+        case 1: e = launch_reduce_raw<1>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
+        case 2: e = launch_reduce_raw<2>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
+        case 4: e = launch_reduce_raw<4>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
+        case 5: e = launch_reduce_raw<5>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
+        case 12: e = launch_reduce_raw<12>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
+    }
+    unsigned long long first = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&first, status, sizeof(first), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(status, s);
+    if (e != cudaSuccess) return cuda_fail(e, "hsad_reduce_raw");
+    if (first != ~0ull) return nonfinite_error(h, first);
+    return HSAD_OK;
+}
+
+extern "C" hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                                      void* d_out, int32_t out_bytes, void* stream) {
+    if (!header) return set_error(HSAD_E_INVALID_VALUE, "null header");
+    const hsad_cube_header& h = *header;
+    hsad_status vst = validate_raw(h, raw_bytes);
+    if (vst != HSAD_OK) return vst;
     if (out_bytes != 8 && out_bytes != 4)
         return set_error(HSAD_E_INVALID_VALUE, "out_bytes must be 8 (fp64) or 4 (fp32)");
     if (out_bytes == 4 && h.data_type_code == 5)
@@ -280,12 +454,6 @@ extern "C" hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, cons
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFreeAsync(status, s);
     if (e != cudaSuccess) return cuda_fail(e, "hsad_read_cube");
-    if (first != ~0ull) {  // cube.cpp:244-247
-        const int64_t band = static_cast<int64_t>(first % h.bands);
-        const int64_t pix = static_cast<int64_t>(first / h.bands);
-        return set_error(HSAD_E_NON_FINITE_VALUE, "at (row=" + std::to_string(pix / h.samples) +
-                                                      ", col=" + std::to_string(pix % h.samples) +
-                                                      ", band=" + std::to_string(band) + ")");
-    }
+    if (first != ~0ull) return nonfinite_error(h, first);  // cube.cpp:244-247
     return HSAD_OK;
 }

@@ -1,6 +1,7 @@
 """Python mirror of the reference's cube ingest and evaluation API over the C-ABI.
 
     read_cube(raw, header)            hsad::read_cube          cube.hpp:70-72, cube.cpp:198-253
+    reduce_raw(raw, header, order, t) read_cube + reduce_cube  (wavelet.cpp:148-167), one pass
     roc_curve(scores, truth)          hsad::roc_curve          eval.hpp:23, eval.cpp:10-57
     auc(curve)                        hsad::auc                eval.hpp:26, eval.cpp:59-67
     adaptive_threshold(scores, z)     hsad::adaptive_threshold eval.hpp:37, eval.cpp:69-90
@@ -54,6 +55,19 @@ def read_cube(raw: torch.Tensor, header: CubeHeader, out_dtype: torch.dtype = to
     out = torch.empty(shape, dtype=out_dtype, device=raw.device)
     _check(_abi.lib().hsad_read_cube(raw.data_ptr(), raw.numel() * raw.element_size(), C.byref(h),
                                      out.data_ptr(), out.element_size(), _stream_ptr()))
+    return out
+
+
+def reduce_raw(raw: torch.Tensor, header: CubeHeader, order: int = 2, target_bands: int = 4,
+               out_dtype: torch.dtype = torch.float64) -> torch.Tensor:
+    """read_cube + reduce_cube in one pass over a raw BSQ / BIL cube (no BIP intermediate)."""
+    raw = _u8(raw, "raw")
+    h = header.to_c()
+    out = torch.empty((max(header.lines, 0), max(header.samples, 0), max(target_bands, 0)),
+                      dtype=out_dtype, device=raw.device)
+    _check(_abi.lib().hsad_reduce_raw(raw.data_ptr(), raw.numel() * raw.element_size(), C.byref(h),
+                                      order, target_bands, out.data_ptr(), out.element_size(),
+                                      _stream_ptr()))
     return out
 
 

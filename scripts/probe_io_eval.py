@@ -41,7 +41,18 @@ for il in ("bsq", "bil"):
         gb = (raw.numel() + cube.numel() * eb) / 1e9
         out[f"read_cube {il} f32->{'f32' if eb == 4 else 'f64'}"] = {"ms": ms, "GB": gb, "GB/s": gb / ms * 1e3}
         del cube
-del raw
+# fused decode + DWT from the raw BSQ / BIL bytes vs read_cube then reduce_cube
+import ctypes as C
+from paper_1201_2025_b200 import _abi
+red = torch.empty((L, S, 4), dtype=torch.float64, device="cuda")
+for il in ("bsq", "bil"):
+    h = evalio.CubeHeader(S, L, B, il, 4, 0).to_c()
+    fn = lambda: _abi.lib().hsad_reduce_raw(raw.data_ptr(), raw.numel(), C.byref(h), 2, 4, red.data_ptr(), 8,
+                                            torch.cuda.current_stream().cuda_stream)
+    ms = timeit(fn)
+    gb = (raw.numel() + red.numel() * 8) / 1e9
+    out[f"reduce_raw {il} f32 -> 4 bands f64"] = {"ms": ms, "GB": gb, "GB/s": gb / ms * 1e3}
+del raw, red
 torch.cuda.empty_cache()
 g = torch.Generator(device="cuda").manual_seed(7)
 scores = torch.empty((L, S), dtype=torch.float64, device="cuda").exponential_(generator=g)

@@ -140,3 +140,33 @@ def test_threshold_and_pgm():
     assert evalio.render_pgm(torch.as_tensor(s).to(DEV)) == want
     c = torch.full((3, 4), 2.5, dtype=torch.float64, device=DEV)
     assert evalio.render_pgm(c) == io.render_pgm(np.full((3, 4), 2.5))
+
+
+@pytest.mark.parametrize("interleave", ["bsq", "bil", "bip"])
+@pytest.mark.parametrize("code,byte_order", [(4, 0), (4, 1), (2, 1), (12, 0), (1, 0), (5, 0)])
+def test_reduce_raw_matches_read_then_reduce(orc, interleave, code, byte_order):
+    """hsad_reduce_raw == reduce_cube(read_cube(raw)) of the oracle (DWT bar 1e-5; we hold
+    1e-10 relative), for every interleave / type / byte order."""
+    lines, samples, bands = 13, 70, 189
+    rng = np.random.default_rng(code * 7 + byte_order + len(interleave))
+    raw = _raw(rng, lines, samples, bands, code, byte_order)
+    cube = io.read_cube(raw, samples, lines, bands, interleave, code, byte_order)
+    want = orc.port.reduce_cube(cube, 2, 4)
+    hdr = evalio.CubeHeader(samples, lines, bands, interleave, code, byte_order)
+    got = evalio.reduce_raw(_dev(raw), hdr, 2, 4).cpu().numpy()
+    assert orc.max_rel_diff(got, want) < 1e-10  # summation order; int16-scale data cancels
+
+
+def test_reduce_raw_errors():
+    z = np.zeros((64, 3, 4), np.float32)  # BSQ: 64 bands of 3 x 4
+    z[10, 2, 1] = np.nan
+    hdr = evalio.CubeHeader(4, 3, 64, "bsq", 4, 0)
+    with pytest.raises(HsadError) as e:
+        evalio.reduce_raw(_dev(z.tobytes()), hdr, 2, 4)
+    assert str(e.value) == "NonFiniteValue: at (row=2, col=1, band=10)"
+    with pytest.raises(HsadError) as e:
+        evalio.reduce_raw(_dev(z.tobytes()), hdr, 11, 4)
+    assert e.value.name == "UnsupportedOrder"
+    with pytest.raises(HsadError) as e:
+        evalio.reduce_raw(_dev(z.tobytes()[:-8]), hdr, 2, 4)
+    assert e.value.name == "SizeMismatch"
