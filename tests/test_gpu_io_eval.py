@@ -144,10 +144,11 @@ def test_threshold_and_pgm():
 
 @pytest.mark.parametrize("interleave", ["bsq", "bil", "bip"])
 @pytest.mark.parametrize("code,byte_order", [(4, 0), (4, 1), (2, 1), (12, 0), (1, 0), (5, 0)])
-def test_reduce_raw_matches_read_then_reduce(orc, interleave, code, byte_order):
+@pytest.mark.parametrize("lines,samples", [(13, 70), (16, 128)])  # (16, 128): the TMA ring path
+def test_reduce_raw_matches_read_then_reduce(orc, interleave, code, byte_order, lines, samples):
     """hsad_reduce_raw == reduce_cube(read_cube(raw)) of the oracle (DWT bar 1e-5; we hold
     1e-10 relative), for every interleave / type / byte order."""
-    lines, samples, bands = 13, 70, 189
+    bands = 189
     rng = np.random.default_rng(code * 7 + byte_order + len(interleave))
     raw = _raw(rng, lines, samples, bands, code, byte_order)
     cube = io.read_cube(raw, samples, lines, bands, interleave, code, byte_order)
@@ -170,3 +171,15 @@ def test_reduce_raw_errors():
     with pytest.raises(HsadError) as e:
         evalio.reduce_raw(_dev(z.tobytes()[:-8]), hdr, 2, 4)
     assert e.value.name == "SizeMismatch"
+
+
+def test_reduce_raw_large_aligned_nonfinite():
+    """A wider aligned BSQ cube: the first non-finite element in (row, col, band) order."""
+    rng = np.random.default_rng(77)
+    cube = rng.normal(0, 2, size=(224, 16, 256)).astype(np.float32)  # BSQ bands x lines x samples
+    hdr = evalio.CubeHeader(256, 16, 224, "bsq", 4, 0)
+    cube[100, 7, 200] = np.inf
+    cube[150, 3, 9] = np.nan
+    with pytest.raises(HsadError) as e:
+        evalio.reduce_raw(_dev(cube.tobytes()), hdr, 2, 4)
+    assert str(e.value) == "NonFiniteValue: at (row=3, col=9, band=150)"
