@@ -41,8 +41,11 @@ def label(i, name, seen):
 def main():
     rep, tag, note = sys.argv[1], sys.argv[2], sys.argv[3]
     first = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # window index of the first detect launch
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):  # already exported with ncu -i <rep> --page raw --csv
+        raw = Path(rep).read_text()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     full, traffic = [], []
