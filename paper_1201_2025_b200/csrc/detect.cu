@@ -808,10 +808,13 @@ template <int L, int NBOX, int K, bool STD, bool ZC>
 // 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
 // fp64 operations, and extra warps hide their latency better than the registers
 // a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
+#ifndef HSAD_DET_NT
+#define HSAD_DET_NT 128  // threads (= output columns at K = 1) per CTA
+#endif
 #ifndef HSAD_DET_MINB
 #define HSAD_DET_MINB 4
 #endif
-__global__ void __launch_bounds__(128, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kernel(const DetectParams P) {
+__global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kernel(const DetectParams P) {
     constexpr int NC = Dim<L>::NC;
     constexpr int NC2 = Dim<L>::NC2;
     constexpr int S2 = Dim<L>::S2;
@@ -1186,7 +1189,7 @@ const char* algo_name(int a) {
 
 struct Plan {
     DetectParams P{};
-    int nt = 128;
+    int nt = HSAD_DET_NT;
     int kcols = 1;
     dim3 grid;
 };
@@ -1296,7 +1299,7 @@ int64_t row_quantum(int64_t lines, int64_t samples) {
     // chunk height: large enough to amortise the 2R+1-row warm-up, small enough
     // that the grid fills the GPU twice (148 SMs); depends on the image only
     const int sms = 148;
-    const int64_t tw = 128 * kcols_for(samples);
+    const int64_t tw = HSAD_DET_NT * kcols_for(samples);
     const int64_t strips = (samples + tw - 1) / tw;
     // 32 measured best on C5 (24..128 sweep: within 1% of 24, 3.6% faster than 64)
     int64_t q = 32;
@@ -1373,16 +1376,20 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     P.chunk = row_quantum(lines, samples);
     // 128 threads x K output columns; shrink K until the per-box vertical sums
     // (strip + halo columns) fit comfortably in shared memory
-    plan.nt = 128;
+    plan.nt = HSAD_DET_NT;
     int kc = bands == 4 ? kcols_for(samples) : 1;
     auto smem_for = [&](int k) {
-        const int64_t ncol = 128 * k + 2 * P.rmax;
+        const int64_t ncol = static_cast<int64_t>(HSAD_DET_NT) * k + 2 * P.rmax;
         const int s2 = ((bands + bands * (bands + 1) / 2 + 1) / 2) | 1;
         return (static_cast<int64_t>(P.nbox) * (ncol * s2 + (k > 1 ? ncol / k + 1 : 0)) +
                 nz_pairs(P.nbox, static_cast<int>(ncol))) * 16;
     };
     // <= 56 KB keeps 4 CTAs per SM (228 KB shared memory); K shrinks to fit
-    const int64_t smem_cap = getenv("HSAD_SMEM_CAP_KB") ? atoi(getenv("HSAD_SMEM_CAP_KB")) * 1024 : 56 * 1024;
+#ifndef HSAD_DET_SMEM_KB
+#define HSAD_DET_SMEM_KB 56
+#endif
+    const int64_t smem_cap = getenv("HSAD_SMEM_CAP_KB") ? atoi(getenv("HSAD_SMEM_CAP_KB")) * 1024
+                                                        : HSAD_DET_SMEM_KB * 1024;
     while (kc > 1 && smem_for(kc) > smem_cap) kc /= 2;
     if (!fullband && smem_for(kc) > 227 * 1024)
         return set_error(HSAD_E_UNSUPPORTED,
@@ -1391,7 +1398,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                              " bands exceed shared memory; split the requests");
     if (fullband) kc = 1;
     plan.kcols = kc;
-    P.tw = 128 * kc;
+    P.tw = HSAD_DET_NT * kc;
     // STD kernel (standard layout, fp64 4-band cube) with the TMA row stage, if the
     // stage fits next to the window sums under the 4-CTA/SM budget
     P.staged = P.std_layout && elem_bytes == 8 && bands == 4 && P.nbox <= 2 &&
