@@ -624,6 +624,7 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
                     for (int a2 = 0; a2 < 8; ++a2) s_corner[a2] = acc[a2][a2];
             }
             __syncthreads();
+            FB_MARK(4);  // diagonal-block factorisation (critical path)
             if (s_bad || jt == LT) break;  // uniform
             if (own && tk == jt && ti > jt) {
                 // forward substitution against L_jj^T, column by column, in place
@@ -644,6 +645,7 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
                     for (int a2 = 0; a2 < 8; ++a2) lp[c2 * CBP + 10 * ti + a2] = acc[a2][c2];
             }
             __syncthreads();
+            FB_MARK(5);  // panel solves
             if (own && tk > jt) {
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {
@@ -663,6 +665,10 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
                         for (int b2 = 0; b2 < 8; ++b2) acc[a2][b2] = fma(-li[a2], lk[b2], acc[a2][b2]);
                 }
             }
+#ifdef HSAD_PHASE_TIMERS
+            __syncthreads();  // probe build only: separates the trailing update
+            FB_MARK(6);
+#endif
         }
         __syncthreads();
         FB_MARK(3);

@@ -18,7 +18,8 @@ s, e = torch.cuda.Event(True), torch.cuda.Event(True)
 s.record(); hs.detect_multi(cube, reqs); e.record(); torch.cuda.synchronize()
 lib.hsad_fb_phase_cycles(buf, 1)
 print("C3 ms", s.elapsed_time(e))
-names = ["offsets+means", "centred Gram", "d+ridge", "Cholesky tail", "panels", "trailing"]
-tot = sum(buf[i] for i in range(6))
+names = ["offsets+means", "centred Gram", "d+ridge", "Cholesky tail", "diag factor", "panels",
+         "trailing update"]
+tot = sum(buf[i] for i in range(7))
 for i, n in enumerate(names):
     print(f"{n:16s} {buf[i]/1e6:10.1f} Mcyc  {100*buf[i]/tot:5.1f}%   per px {buf[i]/1e4:9.0f} cyc")
