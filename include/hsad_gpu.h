@@ -253,6 +253,18 @@ hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, const hsad_cub
                             int32_t order, int32_t target_bands, void* d_out, int32_t out_bytes,
                             void* stream);
 
+/* read_cube + reduce_cube + detect on HOST buffers (the CLI's reduce + detect on an ENVI
+ * file minus file reading): h_raw holds the raw file bytes of a BSQ or BIL cube; row
+ * strips stream to the device (BSQ as 2D copies of the band-plane segments), are decoded
+ * and reduced in one pass, detected and copied back as in hsad_pipeline_host. Errors:
+ * header / size (read_cube), wavelet parameters, request validation, then NonFiniteValue
+ * anywhere in the cube before any detector failure. host_requests' d_scores / d_eigcount
+ * are HOST pointers (lines x samples). Synchronous. */
+hsad_status hsad_pipeline_raw(const void* h_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                              int32_t order, int32_t target_bands,
+                              const hsad_detect_request* host_requests, int32_t n_requests,
+                              hsad_pixel_error* err, void* stream);
+
 /* ---- evaluation on device ------------------------------------ */
 typedef struct hsad_roc_summary {
     uint64_t positives, negatives;

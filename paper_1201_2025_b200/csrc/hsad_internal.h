@@ -78,6 +78,15 @@ hsad_status wavelet_plan(int32_t bands, int32_t order, int32_t target, std::vect
 
 hsad_status window_validate(const hsad_window& w);
 
+// Raw ENVI cube helpers (ingest.cu): header + byte-count validation with the reference's
+// messages, the NonFiniteValue message for a BIP index, and the asynchronous decode + DWT
+// of rows [row0, row1) of a resident BSQ / BIL cube (first non-finite -> *status).
+hsad_status validate_raw(const hsad_cube_header& h, int64_t raw_bytes);
+hsad_status nonfinite_error(const hsad_cube_header& h, unsigned long long first);
+cudaError_t reduce_raw_rows(const hsad_cube_header& h, const void* d_raw, int32_t order, int32_t target,
+                            void* d_out, int32_t out_bytes, unsigned long long* status, cudaStream_t s,
+                            int64_t row0, int64_t row1);
+
 // Device copy of the composed target x bands wavelet map (cached per thread), reduce.cu.
 hsad_status device_wavelet_map(int32_t bands, int32_t order, int32_t target, const double** d_map);
 

@@ -240,6 +240,7 @@ constexpr int kRawGroups = 4;                   // band groups per CTA
 template <int CODE, int TARGET>
 __global__ void __launch_bounds__(kRawThreads * kRawGroups)
     reduce_raw_kernel(const typename Src<CODE>::T* __restrict__ in, bool swap, int R, int64_t C,
+                      int64_t batch0, int64_t c_begin, int64_t c_end,
                       const double* __restrict__ wmap, void* __restrict__ out, int out_bytes,
                       unsigned long long* status) {
     using T = typename Src<CODE>::T;
@@ -249,12 +250,12 @@ __global__ void __launch_bounds__(kRawThreads * kRawGroups)
     for (int i = threadIdx.x; i < TARGET * R; i += blockDim.x) s_w[i] = wmap[i];
     __syncthreads();
     const int tx = threadIdx.x % kRawThreads, g = threadIdx.x / kRawThreads;
-    const int64_t batch = blockIdx.y;
-    const int64_t cbase = static_cast<int64_t>(blockIdx.x) * kRawPix;
+    const int64_t batch = batch0 + blockIdx.y;
+    const int64_t cbase = c_begin + static_cast<int64_t>(blockIdx.x) * kRawPix;
     const T* src = in + batch * R * C + cbase;
     bool live[kRawPPT];
 #pragma unroll
-    for (int m = 0; m < kRawPPT; ++m) live[m] = cbase + tx + m * kRawThreads < C;
+    for (int m = 0; m < kRawPPT; ++m) live[m] = cbase + tx + m * kRawThreads < c_end;
     double acc[kRawPPT][TARGET];
 #pragma unroll
     for (int m = 0; m < kRawPPT; ++m)
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(kRawThreads * kRawGroups)
     __syncthreads();
     // combine the band groups in a fixed order; the CTA's output run is contiguous
     const int64_t o0 = (batch * C + cbase) * TARGET;
-    const int64_t ncols = C - cbase < kRawPix ? C - cbase : kRawPix;
+    const int64_t ncols = c_end - cbase < kRawPix ? c_end - cbase : kRawPix;
     for (int i = threadIdx.x; i < ncols * TARGET; i += blockDim.x) {
         const double v = (s_part[i] + s_part[kRawPix * TARGET + i]) +
                          (s_part[2 * kRawPix * TARGET + i] + s_part[3 * kRawPix * TARGET + i]);
@@ -304,15 +305,21 @@ __global__ void __launch_bounds__(kRawThreads * kRawGroups)
     }
 }
 
+// rows [row0, row1) of a BSQ / BIL cube whose full raw image is at `raw`; the outputs
+// land at their global BIP positions of `out`
 template <int CODE>
 cudaError_t launch_reduce_raw(const hsad_cube_header& h, const void* raw, bool swap, int target,
                               const double* wmap, void* out, int out_bytes,
-                              unsigned long long* status, cudaStream_t s) {
+                              unsigned long long* status, cudaStream_t s, int64_t row0, int64_t row1) {
     const int64_t plane = static_cast<int64_t>(h.lines) * h.samples;
-    const int64_t batches = h.interleave == HSAD_BSQ ? 1 : h.lines;
-    const int64_t C = h.interleave == HSAD_BSQ ? plane : h.samples;
+    const bool bsq = h.interleave == HSAD_BSQ;
+    const int64_t C = bsq ? plane : h.samples;
+    const int64_t batch0 = bsq ? 0 : row0, batches = bsq ? 1 : row1 - row0;
+    const int64_t c_begin = bsq ? row0 * h.samples : 0, c_end = bsq ? row1 * h.samples : h.samples;
     if (batches > 65535) return cudaErrorInvalidConfiguration;
-    const dim3 grid(static_cast<unsigned>((C + kRawPix - 1) / kRawPix), static_cast<unsigned>(batches));
+    if (batches <= 0 || c_end <= c_begin) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>((c_end - c_begin + kRawPix - 1) / kRawPix),
+                    static_cast<unsigned>(batches));
     const size_t smem = (static_cast<size_t>(target) * h.bands +
                          static_cast<size_t>(kRawGroups) * kRawPix * target) * sizeof(double);
     const auto* in = static_cast<const typename Src<CODE>::T*>(raw);
@@ -320,7 +327,8 @@ cudaError_t launch_reduce_raw(const hsad_cube_header& h, const void* raw, bool s
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        kern<<<grid, kRawThreads * kRawGroups, smem, s>>>(in, swap, h.bands, C, wmap, out, out_bytes, status);
+        kern<<<grid, kRawThreads * kRawGroups, smem, s>>>(in, swap, h.bands, C, batch0, c_begin, c_end,
+                                                          wmap, out, out_bytes, status);
         return cudaGetLastError();
     };
     switch (target) {
@@ -347,9 +355,28 @@ int64_t element_size(int code) {  // cube.cpp:22-33
 }  // namespace
 }  // namespace hsad_b200
 
-using namespace hsad_b200;
+namespace hsad_b200 {
+// Asynchronous decode + DWT of rows [row0, row1) of a resident BSQ / BIL raw cube into the
+// matching rows of d_out; the first non-finite element's BIP index goes to *status
+// (atomicMin). Used by hsad_reduce_raw and the raw host pipeline.
+cudaError_t reduce_raw_rows(const hsad_cube_header& h, const void* d_raw, int32_t order, int32_t target,
+                            void* d_out, int32_t out_bytes, unsigned long long* status, cudaStream_t s,
+                            int64_t row0, int64_t row1) {
+    const double* d_map = nullptr;
+    if (device_wavelet_map(h.bands, order, target, &d_map) != HSAD_OK) return cudaErrorInvalidValue;
+    const bool swap = h.byte_order == 1;
+    switch (h.data_type_code) {
+        case 1: return launch_reduce_raw<1>(h, d_raw, swap, target, d_map, d_out, out_bytes, status, s, row0, row1);
+        case 2: return launch_reduce_raw<2>(h, d_raw, swap, target, d_map, d_out, out_bytes, status, s, row0, row1);
+        case 4: return launch_reduce_raw<4>(h, d_raw, swap, target, d_map, d_out, out_bytes, status, s, row0, row1);
+        case 5: return launch_reduce_raw<5>(h, d_raw, swap, target, d_map, d_out, out_bytes, status, s, row0, row1);
+        case 12: return launch_reduce_raw<12>(h, d_raw, swap, target, d_map, d_out, out_bytes, status, s, row0, row1);
+    }
+    return cudaErrorInvalidValue;
+}
+}  // namespace hsad_b200
 
-namespace {
+namespace hsad_b200 {
 // CubeHeader::validate + the byte count (cube.cpp:22-45, 200-203), same order and messages
 hsad_status validate_raw(const hsad_cube_header& h, int64_t raw_bytes) {
     if (h.samples < 1 || h.lines < 1 || h.bands < 1)
@@ -376,7 +403,9 @@ hsad_status nonfinite_error(const hsad_cube_header& h, unsigned long long first)
                                                   ", col=" + std::to_string(pix % h.samples) +
                                                   ", band=" + std::to_string(band) + ")");
 }
-}  // namespace
+}  // namespace hsad_b200
+
+using namespace hsad_b200;
 
 extern "C" hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, const hsad_cube_header* header,
                                        int32_t order, int32_t target_bands, void* d_out,
@@ -406,20 +435,12 @@ extern "C" hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, con
         target_bands != 16)
         return set_error(HSAD_E_UNSUPPORTED, "raw-cube reduction supports 1..16 target bands");
     const double* d_map = nullptr;
-    st = device_wavelet_map(h.bands, order, target_bands, &d_map);
+    st = device_wavelet_map(h.bands, order, target_bands, &d_map);  // plan errors before any launch
     if (st != HSAD_OK) return st;
-    const bool swap = h.byte_order == 1;
     unsigned long long* status = nullptr;
     HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
     HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
-    cudaError_t e = cudaErrorInvalidValue;
-    switch (h.data_type_code) {
-        case 1: e = launch_reduce_raw<1>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
-        case 2: e = launch_reduce_raw<2>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
-        case 4: e = launch_reduce_raw<4>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
-        case 5: e = launch_reduce_raw<5>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
-        case 12: e = launch_reduce_raw<12>(h, d_raw, swap, target_bands, d_map, d_out, out_bytes, status, s); break;
-    }
+    cudaError_t e = reduce_raw_rows(h, d_raw, order, target_bands, d_out, out_bytes, status, s, 0, h.lines);
     unsigned long long first = ~0ull;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&first, status, sizeof(first), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

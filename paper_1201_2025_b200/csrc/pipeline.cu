@@ -235,3 +235,157 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
                            n_requests, nullptr, err, s);
     return st != HSAD_OK ? st : set_error(HSAD_E_CUDA, "pipeline: failing pixel not reproduced");
 }
+
+// hsad_pipeline_raw: the same streamed composition starting from the raw bytes of an
+// ENVI file (read_cube + reduce_cube + detect, cube.cpp:198-253 -> wavelet.cpp:148-167 ->
+// detect.cpp:159-289) for BSQ / BIL cubes of any supported type. Strip i's rows move
+// host -> device into their place of a device copy of the raw image (BSQ: one 2D copy
+// of `bands` plane segments; BIL: one contiguous block), are decoded and reduced in one
+// pass (reduce_raw_rows), and detected / copied back as in hsad_pipeline_host. int16
+// files move half the PCIe bytes of the fp32 cube. A non-finite element anywhere is
+// reported first (read_cube runs before the detectors in the reference).
+extern "C" hsad_status hsad_pipeline_raw(const void* h_raw, int64_t raw_bytes, const hsad_cube_header* header,
+                                         int32_t order, int32_t target_bands,
+                                         const hsad_detect_request* host_requests, int32_t n_requests,
+                                         hsad_pixel_error* err, void* stream) {
+    if (err) {
+        err->code = HSAD_OK;
+        err->row = err->col = -1;
+    }
+    if (!header) return set_error(HSAD_E_INVALID_VALUE, "null header");
+    const hsad_cube_header& h = *header;
+    hsad_status st = validate_raw(h, raw_bytes);
+    if (st != HSAD_OK) return st;
+    if (h.interleave == HSAD_BIP)
+        return set_error(HSAD_E_UNSUPPORTED, "BIP input: decode with hsad_read_cube or use hsad_pipeline_host");
+    if (order <= 0) return set_error(HSAD_E_UNSUPPORTED, "hsad_pipeline_raw reduces (order >= 1)");
+    if (!h_raw) return set_error(HSAD_E_INVALID_VALUE, "null raw buffer");
+    if (n_requests < 1 || n_requests > kMaxCallRequests || !host_requests)
+        return set_error(HSAD_E_INVALID_VALUE, "between 1 and 16 requests per call");
+    st = wavelet_plan(h.bands, order, target_bands, nullptr);
+    if (st != HSAD_OK) return st;
+    if (target_bands != 1 && target_bands != 2 && target_bands != 4 && target_bands != 8 && target_bands != 16)
+        return set_error(HSAD_E_UNSUPPORTED, "raw-cube reduction supports 1..16 target bands");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t lines = h.lines, samples = h.samples;
+    const int64_t npix = lines * samples;
+    const size_t es = static_cast<size_t>(raw_bytes / (npix * h.bands));
+    PipelineCache& c = g_cache;
+    HSAD_CUDA_TRY(c.init());
+    const size_t row_px = static_cast<size_t>(samples);
+    HSAD_CUDA_TRY(c.cube.reserve(static_cast<size_t>(raw_bytes)));
+    HSAD_CUDA_TRY(c.reduced.reserve(static_cast<size_t>(npix) * target_bands * sizeof(double)));
+    hsad_detect_request dev_req[kMaxCallRequests];
+    for (int q = 0; q < n_requests; ++q) {
+        dev_req[q] = host_requests[q];
+        const int sb = host_requests[q].score_bytes;
+        HSAD_CUDA_TRY(c.out[q].reserve(static_cast<size_t>(npix) * (sb == 4 ? 4 : 8)));
+        dev_req[q].d_scores = c.out[q].p;
+        if (host_requests[q].algorithm == HSAD_DWEST && host_requests[q].d_eigcount) {
+            HSAD_CUDA_TRY(c.counts[q].reserve(static_cast<size_t>(npix)));
+            dev_req[q].d_eigcount = static_cast<int8_t*>(c.counts[q].p);
+        } else {
+            dev_req[q].d_eigcount = nullptr;
+        }
+    }
+    st = detect_multi_impl(c.reduced.p, 8, lines, samples, target_bands, 0, lines, 0, 0, dev_req,
+                           n_requests, nullptr, err, s);
+    if (st != HSAD_OK) return st;
+    // two status words: [0] detector failures, [1] first non-finite raw element
+    HSAD_CUDA_TRY(c.status.reserve(2 * sizeof(uint64_t)));
+    uint64_t* d_status = static_cast<uint64_t*>(c.status.p);
+    unsigned long long* d_nonfinite = reinterpret_cast<unsigned long long*>(d_status + 1);
+    HSAD_CUDA_TRY(cudaMemsetAsync(d_status, 0xff, 2 * sizeof(uint64_t), s));
+
+    int64_t rmax = 0;
+    for (int q = 0; q < n_requests; ++q) {
+        const hsad_window& w = host_requests[q].window;
+        const int64_t r = (w.mode == HSAD_WINDOW_SINGLE ? w.single_size : w.outer_size) / 2;
+        rmax = r > rmax ? r : rmax;
+    }
+    const int64_t quantum = row_quantum(lines, samples);
+    int64_t strip = (lines + kMaxStrips - 1) / kMaxStrips;
+    const int64_t row_bytes = samples * h.bands * static_cast<int64_t>(es);
+    const int64_t min_rows = ((8 << 20) + row_bytes - 1) / row_bytes;
+    if (strip < min_rows) strip = min_rows;
+    strip = (strip + quantum - 1) / quantum * quantum;
+    if (strip < quantum) strip = quantum;
+
+    HSAD_CUDA_TRY(cudaEventRecord(c.ev_start, s));
+    HSAD_CUDA_TRY(cudaStreamWaitEvent(c.h2d, c.ev_start, 0));
+    HSAD_CUDA_TRY(cudaStreamWaitEvent(c.d2h, c.ev_start, 0));
+    const size_t plane_bytes = static_cast<size_t>(npix) * es;
+    int64_t d_done = 0;
+    int i = 0;
+    cudaError_t ce = cudaSuccess;
+    for (int64_t r0 = 0; r0 < lines && ce == cudaSuccess; r0 += strip, ++i) {
+        const int64_t r1 = r0 + strip < lines ? r0 + strip : lines;
+        if (h.interleave == HSAD_BSQ) {  // rows [r0, r1) of every band plane
+            const size_t off = static_cast<size_t>(r0) * row_px * es;
+            ce = cudaMemcpy2DAsync(static_cast<char*>(c.cube.p) + off, plane_bytes,
+                                   static_cast<const char*>(h_raw) + off, plane_bytes,
+                                   static_cast<size_t>(r1 - r0) * row_px * es, h.bands,
+                                   cudaMemcpyHostToDevice, c.h2d);
+        } else {  // BIL: lines are contiguous
+            const size_t off = static_cast<size_t>(r0) * row_bytes;
+            ce = cudaMemcpyAsync(static_cast<char*>(c.cube.p) + off, static_cast<const char*>(h_raw) + off,
+                                 static_cast<size_t>(r1 - r0) * row_bytes, cudaMemcpyHostToDevice, c.h2d);
+        }
+        if (ce != cudaSuccess) break;
+        if ((ce = cudaEventRecord(c.ev_h[i], c.h2d)) != cudaSuccess) break;
+        if ((ce = cudaStreamWaitEvent(s, c.ev_h[i], 0)) != cudaSuccess) break;
+        if ((ce = reduce_raw_rows(h, c.cube.p, order, target_bands, c.reduced.p, 8, d_nonfinite, s, r0, r1)) !=
+            cudaSuccess)
+            break;
+        int64_t d1 = r1 == lines ? lines : (r1 - rmax) / quantum * quantum;
+        if (d1 <= d_done) continue;
+        hsad_detect_request part[kMaxCallRequests];
+        for (int q = 0; q < n_requests; ++q) {
+            part[q] = dev_req[q];
+            const int sb = dev_req[q].score_bytes;
+            part[q].d_scores = static_cast<char*>(dev_req[q].d_scores) + d_done * row_px * sb;
+            if (part[q].d_eigcount) part[q].d_eigcount += d_done * row_px;
+        }
+        st = detect_multi_impl(c.reduced.p, 8, lines, samples, target_bands, 0, r1, d_done, d1, part,
+                               n_requests, d_status, err, s);
+        if (st != HSAD_OK) break;
+        if ((ce = cudaEventRecord(c.ev_d[i], s)) != cudaSuccess) break;
+        if ((ce = cudaStreamWaitEvent(c.d2h, c.ev_d[i], 0)) != cudaSuccess) break;
+        const size_t rows_px = static_cast<size_t>(d1 - d_done) * row_px;
+        for (int q = 0; q < n_requests && ce == cudaSuccess; ++q) {
+            const int sb = host_requests[q].score_bytes;
+            ce = cudaMemcpyAsync(static_cast<char*>(host_requests[q].d_scores) + d_done * row_px * sb,
+                                 part[q].d_scores, rows_px * sb, cudaMemcpyDeviceToHost, c.d2h);
+            if (ce == cudaSuccess && part[q].d_eigcount)
+                ce = cudaMemcpyAsync(host_requests[q].d_eigcount + d_done * row_px, part[q].d_eigcount,
+                                     rows_px, cudaMemcpyDeviceToHost, c.d2h);
+        }
+        d_done = d1;
+    }
+    const cudaError_t e1 = cudaStreamSynchronize(c.h2d);
+    const cudaError_t e2 = cudaStreamSynchronize(c.d2h);
+    const cudaError_t e3 = cudaStreamSynchronize(s);
+    if (st != HSAD_OK) return st;
+    HSAD_CUDA_TRY(ce);
+    HSAD_CUDA_TRY(e1);
+    HSAD_CUDA_TRY(e2);
+    HSAD_CUDA_TRY(e3);
+    unsigned long long words[2] = {~0ull, ~0ull};
+    HSAD_CUDA_TRY(cudaMemcpy(words, d_status, sizeof(words), cudaMemcpyDeviceToHost));
+    if (words[1] != ~0ull) return nonfinite_error(h, words[1]);  // read_cube fails first
+    if (words[0] == ~0ull) return HSAD_OK;
+    // a pixel failed: its row chunk again, synchronously, for the reference message
+    const int64_t row = static_cast<int64_t>(words[0] >> 8) / samples;
+    const int64_t a = row / quantum * quantum;
+    const int64_t b = a + quantum < lines ? a + quantum : lines;
+    hsad_detect_request part[kMaxCallRequests];
+    for (int q = 0; q < n_requests; ++q) {
+        part[q] = dev_req[q];
+        const int sb = dev_req[q].score_bytes;
+        part[q].d_scores = static_cast<char*>(dev_req[q].d_scores) + a * row_px * sb;
+        if (part[q].d_eigcount) part[q].d_eigcount += a * row_px;
+    }
+    st = detect_multi_impl(c.reduced.p, 8, lines, samples, target_bands, 0, lines, a, b, part, n_requests,
+                           nullptr, err, s);
+    return st != HSAD_OK ? st : set_error(HSAD_E_CUDA, "pipeline: failing pixel not reproduced");
+}

@@ -2,6 +2,7 @@
 
     read_cube(raw, header)            hsad::read_cube          cube.hpp:70-72, cube.cpp:198-253
     reduce_raw(raw, header, order, t) read_cube + reduce_cube  (wavelet.cpp:148-167), one pass
+    pipeline_raw(host_raw, header, ...) read + reduce + detect from HOST raw bytes (streamed)
     roc_curve(scores, truth)          hsad::roc_curve          eval.hpp:23, eval.cpp:10-57
     auc(curve)                        hsad::auc                eval.hpp:26, eval.cpp:59-67
     adaptive_threshold(scores, z)     hsad::adaptive_threshold eval.hpp:37, eval.cpp:69-90
@@ -69,6 +70,24 @@ def reduce_raw(raw: torch.Tensor, header: CubeHeader, order: int = 2, target_ban
                                       order, target_bands, out.data_ptr(), out.element_size(),
                                       _stream_ptr()))
     return out
+
+
+def pipeline_raw(h_raw, header: CubeHeader, order: int, target_bands: int, requests, outputs):
+    """hsad_pipeline_raw: raw ENVI bytes on the HOST (numpy array / CPU uint8 tensor, pinned
+    recommended) -> streamed decode + DWT + detectors -> host maps. `outputs` is a list of
+    (scores, eigcount-or-None) CPU tensors sized (lines, samples)."""
+    from ._abi import PixelError, Request
+    from .hsad import _make_request
+    buf = h_raw if isinstance(h_raw, torch.Tensor) else torch.from_numpy(h_raw)
+    if buf.is_cuda:
+        raise TypeError("h_raw must be host memory (use reduce_raw for device buffers)")
+    buf = buf.contiguous()
+    h = header.to_c()
+    reqs = (Request * len(requests))(*[_make_request(r, sc, cnt) for r, (sc, cnt) in zip(requests, outputs)])
+    err = PixelError()
+    _check(_abi.lib().hsad_pipeline_raw(buf.data_ptr(), buf.numel() * buf.element_size(), C.byref(h), order,
+                                        target_bands, reqs, len(requests), C.byref(err), _stream_ptr()), err)
+    return outputs
 
 
 def _scores(s) -> torch.Tensor:

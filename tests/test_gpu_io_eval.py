@@ -183,3 +183,42 @@ def test_reduce_raw_large_aligned_nonfinite():
     with pytest.raises(HsadError) as e:
         evalio.reduce_raw(_dev(cube.tobytes()), hdr, 2, 4)
     assert str(e.value) == "NonFiniteValue: at (row=3, col=9, band=150)"
+
+
+@pytest.mark.parametrize("interleave,code,byte_order", [("bsq", 4, 0), ("bil", 2, 1), ("bsq", 12, 1)])
+def test_pipeline_raw_equals_device_path_and_oracle(orc, interleave, code, byte_order):
+    """Host raw ENVI bytes -> hsad_pipeline_raw (streamed strips) == reduce_raw + detect_multi
+    on the device (bit for bit) and the oracle's read -> reduce -> detect (1e-9)."""
+    lines, samples, bands = 700, 97, 64  # 17 MB: three >= 8 MB strips
+    rng = np.random.default_rng(lines + code)
+    raw = _raw(rng, lines, samples, bands, code, byte_order)
+    hdr = evalio.CubeHeader(samples, lines, bands, interleave, code, byte_order)
+    reqs = [hs.DetectRequest("lrx", hs.WindowConfig.single(7)),
+            hs.DetectRequest("dwrx", hs.WindowConfig.dual(3, 9)),
+            hs.DetectRequest("dwest", hs.WindowConfig.dual(3, 9), eigcount=True)]
+    outs = [(torch.empty((lines, samples), dtype=torch.float64),
+             torch.empty((lines, samples), dtype=torch.int8) if r.eigcount else None) for r in reqs]
+    evalio.pipeline_raw(np.frombuffer(raw, np.uint8).copy(), hdr, 2, 4, reqs, outs)
+    red = evalio.reduce_raw(_dev(raw), hdr, 2, 4)
+    dev = hs.detect_multi(red, reqs)
+    for (a, ca), (b, cb) in zip(outs, dev):
+        assert np.array_equal(a.numpy(), b.cpu().numpy())
+        assert (ca is None) == (cb is None) and (ca is None or np.array_equal(ca.numpy(), cb.cpu().numpy()))
+    cube = io.read_cube(raw, samples, lines, bands, interleave, code, byte_order)
+    red_o = orc.port.reduce_cube(cube, 2, 4)
+    assert orc.max_rel_diff(outs[0][0].numpy(), orc.port.local_rx(red_o, 7)) < 1e-9
+    assert orc.max_rel_diff(outs[1][0].numpy(), orc.port.dwrx(red_o, 3, 9)) < 1e-9
+    s_, c_ = orc.port.dwest(red_o, 3, 9)
+    assert orc.max_rel_diff(outs[2][0].numpy(), s_) < 1e-9 and np.array_equal(outs[2][1].numpy(), c_)
+
+
+def test_pipeline_raw_nonfinite_first():
+    z = np.zeros((64, 40, 30), np.float32)  # BSQ
+    z[:, :, :] = np.random.default_rng(3).random((64, 40, 30)).astype(np.float32)
+    z[5, 33, 7] = np.nan
+    hdr = evalio.CubeHeader(30, 40, 64, "bsq", 4, 0)
+    outs = [(torch.empty((40, 30), dtype=torch.float64), None)]
+    with pytest.raises(HsadError) as e:
+        evalio.pipeline_raw(np.frombuffer(z.tobytes(), np.uint8).copy(), hdr, 2, 4,
+                            [hs.DetectRequest("lrx", hs.WindowConfig.single(5))], outs)
+    assert str(e.value) == "NonFiniteValue: at (row=33, col=7, band=5)"
