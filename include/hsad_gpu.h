@@ -217,6 +217,17 @@ hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, int64_t sampl
                                const hsad_detect_request* host_requests, int32_t n_requests,
                                hsad_pixel_error* err, void* stream);
 
+/* One process, G GPUs: the image splits into n_strips row strips aligned to
+ * hsad_row_quantum; strip g runs on device g % deviceCount from its own host thread
+ * (buffer rows = strip + reflected window halo from h_cube, reduce, fused detectors on
+ * the strip's rows) and writes its map rows straight into the HOST maps of host_requests.
+ * Maps are bit-identical to a one-strip run. Errors: the first failing pixel in row-major
+ * order, as one sequential call would report it. Synchronous. */
+hsad_status hsad_pipeline_sharded(const float* h_cube, int64_t lines, int64_t samples, int32_t bands,
+                                  int32_t order, int32_t target_bands,
+                                  const hsad_detect_request* host_requests, int32_t n_requests,
+                                  int32_t n_strips, hsad_pixel_error* err);
+
 /* ---- ENVI ingest --------------------------------------------- */
 typedef enum hsad_interleave { /* hsad::Interleave, cube.hpp:20 */
     HSAD_BSQ = 0,

@@ -38,7 +38,7 @@ EXPORTED = [
     "hsad_device_check", "hsad_mirror_index", "hsad_window_validate", "hsad_daubechies_filters",
     "hsad_reduce", "hsad_detect", "hsad_detect_multi", "hsad_strip_rows", "hsad_row_quantum",
     "hsad_decode_status", "hsad_pipeline_host", "hsad_reduce_detect",
-    "hsad_read_cube", "hsad_reduce_raw", "hsad_pipeline_raw", "hsad_roc", "hsad_top_k", "hsad_adaptive_threshold", "hsad_render_pgm",
+    "hsad_read_cube", "hsad_reduce_raw", "hsad_pipeline_raw", "hsad_pipeline_sharded", "hsad_roc", "hsad_top_k", "hsad_adaptive_threshold", "hsad_render_pgm",
 ]
 
 HSAD_BSQ, HSAD_BIL, HSAD_BIP = 0, 1, 2
@@ -108,6 +108,8 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
         "hsad_reduce_raw": (I32, [VP, I64, P(CubeHeader), I32, I32, VP, I32, VP]),
         "hsad_pipeline_raw": (I32, [VP, I64, P(CubeHeader), I32, I32, P(Request), I32,
                                     P(PixelError), VP]),
+        "hsad_pipeline_sharded": (I32, [VP, I64, I64, I32, I32, I32, P(Request), I32, I32,
+                                        P(PixelError)]),
         "hsad_roc": (I32, [VP, I32, VP, I64, P(RocSummary), VP, VP, I64, VP]),
         "hsad_top_k": (I32, [VP, I32, I64, I64, VP, P(D), VP]),
         "hsad_adaptive_threshold": (I32, [VP, I32, I64, D, P(D), VP, VP]),

@@ -129,3 +129,24 @@ def run_sharded(rows_of: Callable[[int, int], torch.Tensor], lines: int, samples
     else:
         cmaps = [None] * len(requests)
     return plan, maps, cmaps
+
+
+def pipeline_sharded(h_cube: torch.Tensor, order: int, target_bands: int,
+                     requests: Sequence[DetectRequest], outputs, n_strips: int):
+    """hsad_pipeline_sharded: one process, n_strips row strips over the visible GPUs
+    (strip g on device g % count), host fp32 BIP cube in, host maps out (each GPU writes
+    its own rows; no collective). `outputs`: (scores, eigcount-or-None) CPU tensors."""
+    import ctypes as C
+    from . import _abi
+    from .hsad import _check, _make_request
+    if h_cube.is_cuda or h_cube.dtype != torch.float32:
+        raise TypeError("h_cube must be a host float32 tensor")
+    h_cube = h_cube.contiguous()
+    lines, samples, bands = h_cube.shape
+    reqs = (_abi.Request * len(requests))(*[_make_request(r, sc, cnt)
+                                            for r, (sc, cnt) in zip(requests, outputs)])
+    err = _abi.PixelError()
+    _check(_abi.lib().hsad_pipeline_sharded(h_cube.data_ptr(), lines, samples, bands, order,
+                                            target_bands, reqs, len(requests), n_strips,
+                                            C.byref(err)), err)
+    return outputs

@@ -97,3 +97,12 @@ def test_limits():
     lim = _abi.Limits()
     _abi.lib().hsad_get_limits(C.byref(lim))
     assert lim.max_detect_bands >= 4 and lim.max_window >= 21 and lim.max_reduce_bands >= 224
+
+
+def test_pipeline_sharded_validates_on_host():
+    lib = _abi.lib()
+    req = (_abi.Request * 1)(_abi.Request(_abi.HSAD_LRX, _abi.Window(0, 5, 0, 0), 1, 1e-6, 0.1,
+                                          None, 8, None))
+    e = _abi.PixelError()
+    assert lib.hsad_pipeline_sharded(None, 4, 4, 8, 2, 4, req, 1, 0, C.byref(e)) == _abi.HSAD_E_INVALID_VALUE
+    assert lib.hsad_last_error_message() == b"InvalidValue: n_strips must be >= 1"

@@ -688,3 +688,40 @@ def test_maximum_window_and_limits(orc):
     with pytest.raises(hs.HsadError) as e:
         run(cube, [hs.DetectRequest("lrx", W1(w + 2))])
     assert e.value.name == "Unsupported"
+
+
+@pytest.mark.parametrize("n_strips", [1, 2, 3, 5])
+def test_pipeline_sharded_equals_pipeline_host(orc, n_strips):
+    """hsad_pipeline_sharded (strip g on device g % count: all on this one GPU here) writes
+    maps bit-identical to the single-strip host pipeline, and the oracle's."""
+    from paper_1201_2025_b200.sharded import pipeline_sharded
+    cube = torch.as_tensor(orc.port.random_cube(203, 150, 64, 31).astype(np.float32))
+    reqs = [hs.DetectRequest("lrx", W1(9)), hs.DetectRequest("dwrx", W2(3, 9)),
+            hs.DetectRequest("dwest", W2(3, 9), eigcount=True)]
+    mk = lambda: [(torch.empty((203, 150), dtype=torch.float64),  # noqa: E731
+                   torch.empty((203, 150), dtype=torch.int8) if r.eigcount else None) for r in reqs]
+    want, got = mk(), mk()
+    hs.pipeline_host(cube, 2, 4, reqs, want)
+    pipeline_sharded(cube, 2, 4, reqs, got, n_strips)
+    for (a, ca), (b, cb) in zip(got, want):
+        assert np.array_equal(a.numpy(), b.numpy())
+        assert (ca is None) == (cb is None) and (ca is None or np.array_equal(ca.numpy(), cb.numpy()))
+    red_o = orc.port.reduce_cube(cube.numpy().astype(np.float64), 2, 4)
+    assert max_rel_diff(got[0][0].numpy(), orc.port.local_rx(red_o, 9)) < TOL64
+
+
+def test_pipeline_sharded_error_is_first_pixel(orc):
+    from paper_1201_2025_b200.sharded import pipeline_sharded
+    cube = orc.port.random_cube(400, 40, 64, 12).astype(np.float32)
+    cube[300:320] = 0.0
+    cube[310, 20] = 1.0   # singular background in a later strip
+    cube[350:370] = 0.0
+    cube[360, 5] = 1.0
+    reqs = [hs.DetectRequest("lrx", W1(3))]
+    outs = [(torch.empty((400, 40), dtype=torch.float64), None)]
+    with pytest.raises(hs.HsadError) as want:
+        hs.pipeline_host(torch.as_tensor(cube), 2, 4, reqs, outs)
+    with pytest.raises(hs.HsadError) as got:
+        pipeline_sharded(torch.as_tensor(cube), 2, 4, reqs, outs, 4)
+    assert (got.value.name, got.value.row, got.value.col) == (want.value.name, want.value.row, want.value.col)
+    assert str(got.value) == str(want.value)
