@@ -443,7 +443,9 @@ def run_b200(args, cfg, rank, world, local, dist):
             },
         },
         "clocks": clk,
-        "gpu_launches": (1 + len(SWEEP)) * args.steps,
+        # per step: 1 reduce + per window pair a fast detector pass and its zero-window
+        # counting pass (which exits at once on data without all-zero spectra)
+        "gpu_launches": (1 + 2 * len(SWEEP)) * args.steps,
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline and host_cube is not None:
