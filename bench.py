@@ -261,7 +261,8 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        if args.impl == "b200":  # the reference arm is CPU-only (gloo)
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
