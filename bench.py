@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     return ap.parse_args()
 
 
@@ -173,39 +174,179 @@ def cpu_baseline(cube_rows_np: np.ndarray, lines: int, rows_total: int, budget_s
                       f"with {cores} threads"}
 
 
+# ---- parity gate on the benchmarked workload (a deterministic subset) ----------
+
+def mirror(i: int, n: int) -> int:
+    """mirror_index (proj/core/src/detect.cpp:71-76)."""
+    if n == 1:
+        return 0
+    p = 2 * (n - 1)
+    i = abs(i) % p
+    return i if i < n else p - i
+
+
+def parity_rows(lines: int, quantum: int, rmax: int = RMAX, n_random: int = 64,
+                seed: int = 0x1201) -> list[int]:
+    """SURVEY 8d's C5 subset: the top border rows 0..R+q (the first chunk and its
+    warm-up), every shard-boundary row +-R for G in {2, 4, 8}, the last row of a few
+    chunks (longest running-sum chain), n_random seeded random rows, the last R+1 rows."""
+    rows = set(range(0, min(lines, rmax + quantum + 1)))
+    for g in (2, 4, 8):
+        per = -(-lines // (g * quantum)) * quantum
+        for k in range(1, g):
+            b = k * per
+            rows.update(r for r in range(b - rmax, b + rmax + 1) if 0 <= r < lines)
+    rows.update(r for r in (quantum - 1, 2 * quantum - 1, lines // 2 - 1) if 0 <= r < lines)
+    rng = np.random.default_rng(seed)
+    rows.update(int(r) for r in rng.integers(0, lines, n_random))
+    rows.update(range(max(0, lines - rmax - 1), lines))
+    return sorted(rows)
+
+
+def runs_of(rows):
+    out, s = [], None
+    for i, r in enumerate(rows):
+        if s is None:
+            s = r
+        if i + 1 == len(rows) or rows[i + 1] != r + 1:
+            out.append((s, r + 1))
+            s = None
+    return out
+
+
+def topk_check(gpu: np.ndarray, ref: np.ndarray, k: int):
+    """Identical top-k pixel sets (k = truth positives), plus the oracle's k/k+1 margin."""
+    if k <= 0 or k >= gpu.size:
+        return True, None
+    g = np.argsort(-gpu.ravel(), kind="stable")[:k]
+    o_order = np.argsort(-ref.ravel(), kind="stable")
+    o = o_order[:k]
+    margin = float(ref.ravel()[o_order[k - 1]] - ref.ravel()[o_order[k]])
+    return bool(set(g.tolist()) == set(o.tolist())), margin
+
+
+def oracle_parity(host_cube: np.ndarray, lines: int, rows: list[int], reduced_gpu_rows,
+                  maps_gpu_rows, truth_rows: np.ndarray, cores: int, rmax: int = RMAX,
+                  sweep=SWEEP):
+    """Compares the GPU step's outputs on `rows` with the oracle (oracle/hsad_oracle.cpp).
+
+    host_cube: the fp32 (lines, samples, bands) input; reduced_gpu_rows(r0, r1) -> the
+    GPU's reduced rows; maps_gpu_rows[i](rows) -> map i on `rows` ((scores, counts|None)
+    in the order of requests()). Returns the JSON `parity` block."""
+    import oracle
+    t0 = time.perf_counter()
+    samples = host_cube.shape[1]
+    need = sorted({mirror(r + d, lines) for r in rows for d in range(-rmax, rmax + 1)})
+    red = np.zeros((lines, samples, 4), np.float64)
+    dwt_err = 0.0
+    for a, b in runs_of(need):
+        red[a:b] = oracle.port.reduce_cube(host_cube[a:b], 2, 4, workers=cores)
+        dwt_err = max(dwt_err, oracle.max_rel_diff(reduced_gpu_rows(a, b), red[a:b]))
+    runs = runs_of(rows)
+    names, errs, cnt_bad, topk, ties = [], [], [], [], {}
+    i = 0
+    for inner, outer in sweep:
+        ref_maps = [np.concatenate([oracle.port.local_rx(red, outer, 1e-6, workers=cores, rows=ab)
+                                    for ab in runs]),
+                    np.concatenate([oracle.port.dwrx(red, inner, outer, 1e-6, workers=cores, rows=ab)
+                                    for ab in runs])]
+        ds = [oracle.port.dwest(red, inner, outer, 0.1, workers=cores, rows=ab) for ab in runs]
+        ref_maps.append(np.concatenate([s for s, _ in ds]))
+        ref_cnt = np.concatenate([c for _, c in ds])
+        for algo, ref in zip(("lrx", "dwrx", "dwest"), ref_maps):
+            gs, gc = maps_gpu_rows[i](rows)
+            names.append(f"{algo} {inner}/{outer}" if algo != "lrx" else f"lrx {outer}")
+            errs.append(oracle.max_rel_diff(gs, ref))
+            same, margin = topk_check(gs, ref, int(truth_rows.sum()))
+            topk.append({"identical": same, "oracle_k_margin": margin})
+            if gc is not None:
+                cnt_bad.append(int((gc != ref_cnt).sum()))
+            i += 1
+        mg = [oracle.port.dwest_margins(red, inner, outer, 0.1, workers=cores, rows=ab)
+              for ab in runs]
+        cm = np.concatenate([c for c, _ in mg])
+        sm = np.concatenate([s for _, s in mg])
+        ties[f"{inner}/{outer}"] = {"cutoff_margin_lt_1e-12": int((cm < 1e-12).sum()),
+                                    "sign_margin_lt_1e-12": int((sm < 1e-12).sum()),
+                                    "cutoff_margin_lt_1e-9": int((cm < 1e-9).sum()),
+                                    "min_cutoff_margin": float(cm.min()),
+                                    "min_sign_margin": float(sm.min())}
+    npx = len(rows) * samples
+    gate = (dwt_err <= 1e-5 and max(errs) <= 1e-9 and not any(cnt_bad)
+            and all(t["identical"] for t in topk))
+    return {"pass": bool(gate), "rows": len(rows), "pixels": npx,
+            "row_set": "0..R+q, shard boundaries +-R for G in {2,4,8}, chunk ends, "
+                       "64 seeded random rows, last R+1 rows (SURVEY 8d)",
+            "dwt_max_rel_diff": dwt_err,
+            "max_rel_diff": dict(zip(names, errs)),
+            "bar": "rel_diff |a-b|/max(1,|a|,|b|) (testutil.hpp:34-36) <= 1e-9 fp64 maps, "
+                   "DWT <= 1e-5, identical eigen-counts and top-k",
+            "eigcount_mismatches": cnt_bad,
+            "topk_identical": [t["identical"] for t in topk],
+            "topk_k": int(truth_rows.sum()),
+            "topk_oracle_margin_min": min((t["oracle_k_margin"] for t in topk
+                                           if t["oracle_k_margin"] is not None), default=None),
+            "dwest_near_ties": ties,
+            "oracle": "oracle/hsad_oracle.cpp (pinned to the reference's own code, tests/test_oracle_pin.py)",
+            "seconds": time.perf_counter() - t0}
+
+
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the CPU restatement of the reference path on the host cores."""
+    """--impl reference: the CPU restatement of the reference path (the reference's
+    Eigen build cannot be compiled here) on the host cores, on the same bytes as the
+    GPU arm (host generator) and the same workload. A step is a bounded sample: the
+    DWT of the rows the sample's windows need (timed, then scaled to the sample's own
+    rows so halo rows are not over-counted) + the 12 maps of 8 border and 8 interior
+    output rows."""
     if rank != 0:
         return
-    from harness.scene import generate_rows
-    sample_rows = 16
-    cube = generate_rows(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], 0,
-                         sample_rows + 2 * RMAX + 1, cfg["rate"], device="cpu").numpy()
+    from harness.scene import generate_rows_np
     import oracle
     cores = os.cpu_count() or 1
-    n = sample_rows
+    lines, samples, bands = cfg["lines"], cfg["samples"], cfg["bands"]
+    half = 8
+    mid = lines // 2
+    bands_rows = [(0, half), (mid, mid + half)]  # border rows and interior rows
+    cubes = []
+    for a, b in bands_rows:
+        lo, hi = max(0, a - RMAX), min(lines, b + RMAX)
+        cubes.append((a - lo, b - lo, generate_rows_np(lines, samples, bands, cfg["seed"], lo, hi,
+                                                      cfg["rate"])))
+    n_out = sum(b - a for a, b in bands_rows)
 
     def step():
-        oracle_step(oracle, cube, n, cores)
+        t_red = t_det = 0.0
+        for a, b, cube in cubes:
+            t0 = time.perf_counter()
+            red = oracle.port.reduce_cube(cube, 2, 4, workers=cores)
+            t1 = time.perf_counter()
+            for inner, outer in SWEEP:
+                oracle.port.local_rx(red, outer, 1e-6, workers=cores, rows=(a, b))
+                oracle.port.dwrx(red, inner, outer, 1e-6, workers=cores, rows=(a, b))
+                oracle.port.dwest(red, inner, outer, 0.1, workers=cores, rows=(a, b))
+            t2 = time.perf_counter()
+            t_red += (t1 - t0) * (b - a) / cube.shape[0]  # DWT cost of the output rows only
+            t_det += t2 - t1
+        return t_red + t_det
 
     for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
-    px = n * cfg["samples"]
+    dt = sum(step() for _ in range(args.steps)) / args.steps
+    px = n_out * samples
     v = px / dt / 1e6
     line = {
         "impl": "reference", "metric": "Mpixels/sec for DWT+LRX/DWRX/DWEST scoring",
         "value": v, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, cfg),
+        "config": run_config(args, cfg, world),
         "cpu_baseline": {"value": v, "unit": "Mpixel/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} rows x {cfg['samples']} cols per step (DWT + 3 detectors x 4 "
-                                   "window pairs) of the workload; CPU restatement (the reference "
-                                   "needs Eigen3, absent)"},
+                         "sample": f"per step: output rows {bands_rows} ({px} px, border + interior) "
+                                   f"x 12 maps (LRX/DWRX/DWEST at 4 window pairs) + their DWT "
+                                   f"(timed on the rows the windows need, scaled to the output "
+                                   f"rows); same bytes as the GPU arm (harness/scene_gen.cpp); "
+                                   f"CPU restatement oracle/hsad_oracle.cpp, {cores} threads "
+                                   f"(the reference needs Eigen3, absent)"},
         "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -236,6 +377,11 @@ def detector_ncu():
             "ncu_fp64_tflops_executed": [fp64_tflops(k) for k in det],
             "fp64_peak_tflops_measured": 35.4,
             "ncu_source": "profiles/ncu_full_r1_sweep_d.json (fast passes of the 7/3, 11/5, 15/5, 21/7 detectors)"}
+
+
+def run_config(args, cfg, world):
+    """`config` of both arms (identical keys and values: the driver compares them)."""
+    return dict(workload_config(args, cfg), parallelism=f"row-strips x{world}")
 
 
 def workload_config(args, cfg):
@@ -286,7 +432,11 @@ def run_b200(args, cfg, rank, world, local, dist):
     from paper_1201_2025_b200.sharded import plan_strip
     plan = plan_strip(lines, samples, world, rank, reqs)
     q, per, r0, r1, b0, nb = plan.quantum, plan.per, plan.r0, plan.r1, plan.b0, plan.nb
-    cube = generate_rows(lines, samples, bands, cfg["seed"], b0, b0 + nb, cfg["rate"], device=dev)
+    # the strip's rows are generated on the host (identical bytes to the reference arm and
+    # the parity oracle) into pinned memory: the e2e leg streams from this copy
+    host_cube = generate_rows(lines, samples, bands, cfg["seed"], b0, b0 + nb, cfg["rate"],
+                              pin=True)
+    cube = host_cube.to(dev)
     red = torch.empty((nb, samples, 4), dtype=torch.float64, device=dev)
     # maps live in padded (per, samples) buffers: the strip's rows come first, so at N > 1
     # they are the NCCL send buffers themselves (no staging copy)
@@ -369,10 +519,8 @@ def run_b200(args, cfg, rank, world, local, dist):
 
     # ---- end to end through the C-ABI from pinned host buffers (rank 0 strip only at N>1)
     e2e = None
-    host_cube = None
+    host_out = None
     if rank == 0 or world == 1:
-        host_cube = torch.empty((nb, samples, bands), dtype=torch.float32, pin_memory=True)
-        host_cube.copy_(cube)
         host_out = [(torch.empty((nb, samples), dtype=torch.float64, pin_memory=True),
                      torch.empty((nb, samples), dtype=torch.int8, pin_memory=True) if r.eigcount
                      else None) for r in reqs]
@@ -426,8 +574,8 @@ def run_b200(args, cfg, rank, world, local, dist):
         "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args, cfg), parallelism=f"row-strips x{world}",
-                       row_quantum=q, strip_rows=per),
+        "config": run_config(args, cfg, world),
+        "launch": {"row_quantum": q, "strip_rows": per},
         "roofline": {
             "bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
             "frac": step_gbs / peak, "traffic": traffic, "traffic_unit": traffic_src,
@@ -449,8 +597,29 @@ def run_b200(args, cfg, rank, world, local, dist):
         "gpu_launches": (1 + 2 * len(SWEEP)) * args.steps,
         "e2e": e2e,
     }
-    if world == 1 and not args.no_cpu_baseline and host_cube is not None:
+    if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(host_cube.numpy(), lines, nb, args.cpu_seconds)
+    if world == 1 and not args.no_parity:
+        from harness.scene import anomaly_fill
+        rows = parity_rows(lines, q)
+        idx = torch.tensor(rows)
+        truth, _ = anomaly_fill(lines, samples, cfg["rate"], cfg["seed"])
+        maps = []
+        for (sc, cnt), (hsc, hcnt) in zip(outs, host_out):
+            def get(rws, sc=sc, cnt=cnt):
+                return (sc[idx.to(dev)].cpu().numpy(),
+                        None if cnt is None else cnt[idx.to(dev)].cpu().numpy())
+            maps.append(get)
+        par = oracle_parity(host_cube.numpy(), lines, rows,
+                            lambda a, b: red[a:b].cpu().numpy(), maps, truth[rows],
+                            os.cpu_count() or 1)
+        # the e2e leg (hsad_pipeline_host, pinned host buffers) must reproduce the
+        # device-resident maps bit for bit (quantum-aligned row strips)
+        par["e2e_maps_bit_identical"] = all(
+            torch.equal(sc.cpu(), hsc) and (cnt is None or torch.equal(cnt.cpu(), hcnt))
+            for (sc, cnt), (hsc, hcnt) in zip(outs, host_out))
+        par["pass"] = par["pass"] and par["e2e_maps_bit_identical"]
+        line["parity"] = par
     print(json.dumps(line), flush=True)
 
 

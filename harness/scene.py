@@ -9,72 +9,115 @@ pixels, blend a 6th endmember, z = (1 - f) b + f e6 with f ~ U[0.3, 1.0] (the
 Eq. 10 sub-pixel model, proj/core/src/synth.cpp:20-27); the truth mask marks the
 cluster pixels. fp32 BIP output.
 
-Rows are generated in fixed 64-row chunks, each from its own seeded torch
-generator, so any row range (a rank's strip + halo) is reproduced byte for byte
-on the same device type, independent of how the image is split.
+The bytes come from the host generator harness/scene_gen.cpp (xoshiro256++ per row,
+the algorithm of proj/core/include/hsad/rng.hpp:13-64), so the GPU arm, the CPU
+reference arm and the parity tests consume identical cubes, and any row range (a
+rank's strip + halo, a parity sample) is reproduced byte for byte on its own.
 """
 from __future__ import annotations
 
-import math
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
 
+import numpy as np
 import torch
 
-CHUNK = 64
+HERE = Path(__file__).resolve().parent
+_SO = HERE / "_build" / "libscene.so"
+_lib = None
 
 
-def endmembers(bands: int, seed: int) -> torch.Tensor:
-    g = torch.Generator().manual_seed(seed)
-    p = torch.rand((6, 3, 3), generator=g, dtype=torch.float64)
-    c = p[..., 0] * bands
-    w = 5.0 + 35.0 * p[..., 1]
-    a = 0.1 + 0.9 * p[..., 2]
-    b = torch.arange(bands, dtype=torch.float64)
-    e = (a[..., None] * torch.exp(-(((b - c[..., None]) / w[..., None]) ** 2))).sum(1)
-    return e  # (6, bands)
+def _scene_lib():
+    global _lib
+    if _lib is None:
+        if not _SO.exists():
+            subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+        lib = C.CDLL(str(_SO))
+        D, L, I, U = C.POINTER(C.c_double), C.c_int64, C.c_int, C.c_uint64
+        lib.scene_endmembers.argtypes = [I, U, D]
+        lib.scene_clusters.restype = L
+        lib.scene_clusters.argtypes = [L, L, C.c_double, U, L, C.POINTER(L), C.POINTER(L),
+                                       C.POINTER(C.c_int32), D]
+        lib.scene_rows.argtypes = [L, L, I, U, L, L, D, D, C.c_double, C.POINTER(C.c_float), I]
+        _lib = lib
+    return _lib
 
 
-def anomaly_plan(lines: int, samples: int, rate: float, seed: int):
-    """Cluster pixels (row, col) and their fill fractions, plus the truth mask."""
-    g = torch.Generator().manual_seed(seed ^ 0x5EED)
-    npix = lines * samples
-    n_clusters = max(1, int(round(rate * npix / 2.0)))
-    rows = torch.randint(0, lines, (n_clusters,), generator=g)
-    cols = torch.randint(0, samples, (n_clusters,), generator=g)
-    sizes = torch.randint(1, 4, (n_clusters,), generator=g)
-    fracs = 0.3 + 0.7 * torch.rand((n_clusters,), generator=g, dtype=torch.float64)
-    truth = torch.zeros((lines, samples), dtype=torch.uint8)
-    fill = torch.zeros((lines, samples), dtype=torch.float64)
-    offsets = [(0, 0), (0, 1), (1, 0)]
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def endmembers(bands: int, seed: int) -> np.ndarray:
+    e = np.empty((6, bands), np.float64)
+    _scene_lib().scene_endmembers(bands, seed, _dp(e))
+    return e
+
+
+def clusters(lines: int, samples: int, rate: float, seed: int):
+    lib = _scene_lib()
+    n = int(lib.scene_clusters(lines, samples, rate, seed, 0, None, None, None, None))
+    rows = np.empty(n, np.int64); cols = np.empty(n, np.int64)
+    sizes = np.empty(n, np.int32); fracs = np.empty(n, np.float64)
+    P = C.POINTER
+    lib.scene_clusters(lines, samples, rate, seed, n, rows.ctypes.data_as(P(C.c_int64)),
+                       cols.ctypes.data_as(P(C.c_int64)), sizes.ctypes.data_as(P(C.c_int32)),
+                       _dp(fracs))
+    return rows, cols, sizes, fracs
+
+
+_OFFSETS = [(0, 0), (0, 1), (1, 0)]
+
+
+def anomaly_fill(lines: int, samples: int, rate: float, seed: int, row0: int = 0,
+                 row1: int | None = None):
+    """Truth mask and blend fraction of rows [row0, row1) (later clusters overwrite)."""
+    row1 = lines if row1 is None else row1
+    truth = np.zeros((row1 - row0, samples), np.uint8)
+    fill = np.zeros((row1 - row0, samples), np.float64)
+    rows, cols, sizes, fracs = clusters(lines, samples, rate, seed)
     for r, c, s, f in zip(rows.tolist(), cols.tolist(), sizes.tolist(), fracs.tolist()):
-        for dr, dc in offsets[:s]:
+        for dr, dc in _OFFSETS[:s]:
             rr, cc = r + dr, c + dc
-            if rr < lines and cc < samples:
-                truth[rr, cc] = 1
-                fill[rr, cc] = f
+            if row0 <= rr < row1 and cc < samples:
+                truth[rr - row0, cc] = 1
+                fill[rr - row0, cc] = f
     return truth, fill
 
 
-def generate_rows(lines: int, samples: int, bands: int, seed: int, row0: int, row1: int,
-                  rate: float = 0.002, device="cpu", noise: float = 0.01) -> torch.Tensor:
-    """Rows [row0, row1) of the scene as an fp32 (rows, samples, bands) tensor."""
-    e = endmembers(bands, seed).to(device=device, dtype=torch.float32)
-    _, fill = anomaly_plan(lines, samples, rate, seed)
-    out = torch.empty((row1 - row0, samples, bands), dtype=torch.float32, device=device)
-    k0, k1 = row0 // CHUNK, (row1 + CHUNK - 1) // CHUNK
-    for k in range(k0, k1):
-        a, b = k * CHUNK, min((k + 1) * CHUNK, lines)
-        g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + k + 1)
-        u = torch.rand((b - a, samples, 5), generator=g, device=device, dtype=torch.float32)
-        alpha = -torch.log(u.clamp_min(1e-12))
-        alpha = alpha / alpha.sum(-1, keepdim=True)
-        bg = alpha @ e[:5]
-        bg += noise * torch.randn((b - a, samples, bands), generator=g, device=device,
-                                  dtype=torch.float32)
-        f = fill[a:b].to(device=device, dtype=torch.float32)[..., None]
-        bg = (1.0 - f) * bg + f * e[5]
-        lo, hi = max(a, row0), min(b, row1)
-        out[lo - row0: hi - row0] = bg[lo - a: hi - a]
+def anomaly_plan(lines: int, samples: int, rate: float, seed: int):
+    truth, fill = anomaly_fill(lines, samples, rate, seed)
+    return torch.from_numpy(truth), torch.from_numpy(fill)
+
+
+def generate_rows_np(lines: int, samples: int, bands: int, seed: int, row0: int, row1: int,
+                     rate: float = 0.002, noise: float = 0.01, out: np.ndarray | None = None,
+                     threads: int | None = None) -> np.ndarray:
+    """Rows [row0, row1) of the scene as an fp32 (rows, samples, bands) numpy array."""
+    e = endmembers(bands, seed)
+    _, fill = anomaly_fill(lines, samples, rate, seed, row0, row1)
+    if out is None:
+        out = np.empty((row1 - row0, samples, bands), np.float32)
+    assert out.shape == (row1 - row0, samples, bands) and out.dtype == np.float32
+    assert out.flags.c_contiguous
+    threads = threads or os.cpu_count() or 1
+    _scene_lib().scene_rows(lines, samples, bands, seed, row0, row1, _dp(e), _dp(fill), noise,
+                            out.ctypes.data_as(C.POINTER(C.c_float)), threads)
     return out
+
+
+def generate_rows(lines: int, samples: int, bands: int, seed: int, row0: int, row1: int,
+                  rate: float = 0.002, device="cpu", noise: float = 0.01,
+                  pin: bool = False) -> torch.Tensor:
+    """Rows [row0, row1) of the scene as an fp32 (rows, samples, bands) tensor on `device`
+    (generated on the host: identical bytes on every device)."""
+    host = torch.empty((row1 - row0, samples, bands), dtype=torch.float32,
+                       pin_memory=pin and torch.cuda.is_available())
+    generate_rows_np(lines, samples, bands, seed, row0, row1, rate, noise, out=host.numpy())
+    if torch.device(device).type == "cpu":
+        return host
+    return host.to(device)
 
 
 def generate_scene(lines: int, samples: int, bands: int, seed: int, rate: float = 0.002,

@@ -6,6 +6,7 @@
 // (window validation + mirror), proj/core/src/wavelet.cpp:16-146 (taps, stage,
 // padding, cascade and their error contract).
 #include <bit>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -14,6 +15,38 @@
 #include "hsad_internal.h"
 
 namespace hsad_b200 {
+
+// Library-owned stream-ordered pools, one per device, created on first use.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (static_cast<int>(pools.size()) <= dev) pools.resize(dev + 1, nullptr);
+        if (!pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.handleTypes = cudaMemHandleTypeNone;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            e = cudaMemPoolCreate(&pools[dev], &props);
+            if (e != cudaSuccess) return e;
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = pools[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes > 0 ? bytes : 1, pool, s);
+}
+
+void scratch_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -250,8 +283,8 @@ hsad_status hsad_decode_status(uint64_t packed, int64_t samples, hsad_pixel_erro
         err->row = err->col = -1;
         return HSAD_OK;
     }
-    const uint64_t lin = packed >> 8;
-    err->code = static_cast<int32_t>(packed & 0xff);
+    const uint64_t lin = static_cast<uint64_t>(failure_pixel(packed));
+    err->code = failure_code(packed);
     err->row = static_cast<int64_t>(lin / static_cast<uint64_t>(samples));
     err->col = static_cast<int64_t>(lin % static_cast<uint64_t>(samples));
     return static_cast<hsad_status>(err->code);

@@ -89,7 +89,9 @@ struct DetectParams {
     int has_dual;
     double n_in, n_ann;  // standard-layout dual counts
     unsigned long long* status;
-    int64_t diag_lin;   // >= 0: pixel whose ridge delta is written to diag_out
+    int req_base;       // position of req[0] in the call's request list (failure ordering)
+    int64_t diag_lin;   // >= 0: pixel whose ridge delta is written to diag_out ...
+    int diag_req;       // ... by this request (call position) only
     double* diag_out;
 };
 
@@ -108,12 +110,10 @@ __host__ __device__ inline int nz_pairs(int nbox, int ncol) { return (nbox * nco
 // (possibly from rounding residue in all-zero windows) are suppressed.
 __shared__ int s_zero_seen;
 
-__device__ __forceinline__ void report(const DetectParams& P, int64_t row, int64_t col, int code) {
+__device__ __forceinline__ void report(const DetectParams& P, int q, int64_t row, int64_t col,
+                                       int code) {
     if (s_zero_seen) return;
-    const unsigned long long packed =
-        (static_cast<unsigned long long>(row * P.samples + col) << 8) |
-        static_cast<unsigned long long>(code);
-    atomicMin(P.status, packed);
+    atomicMin(P.status, pack_failure(P.req_base + q, row * P.samples + col, code));
 }
 
 // Reflection on int32 coordinates with the in-range case first (detect.cpp:71-76).
@@ -571,12 +571,12 @@ __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s
 
 // LRX (detect.cpp:168-188) on background sums bg, count n: score = max(d^T (C+dI)^-1 d, 0)
 template <int L>
-__device__ __forceinline__ void lrx_solve(const DetectParams& P, const ReqDev& R,
+__device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const ReqDev& R,
                                           const double (&bg)[Dim<L>::NC], double n_bg, bool bg_zero,
                                           int nzc, const double (&yc)[L], int64_t r, int64_t col,
                                           int64_t o, int64_t lin) {
     if (bg_zero) {  // C = 0, delta = 0: d = 0 -> 0 (detect.cpp:175-177), else singular
-        if (nzc) report(P, r, col, HSAD_E_SINGULAR_AFTER_RIDGE);
+        if (nzc) report(P, q, r, col, HSAD_E_SINGULAR_AFTER_RIDGE);
         store_score(R, o, 0.0);
         return;
     }
@@ -592,9 +592,9 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, const ReqDev& R
     if (dmax > 0.0) {
         double delta = 0.0;
         const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
-        if (lin == P.diag_lin) *P.diag_out = delta;
+        if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
-            report(P, r, col, code);
+            report(P, q, r, col, code);
             score = 0.0;
         }
     }
@@ -632,7 +632,7 @@ __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
 
 // DWRX (detect.cpp:204-223): |m^T (C_ann + dI)^-1 m|
 template <int L>
-__device__ __forceinline__ void dwrx_solve(const DetectParams& P, const ReqDev& R,
+__device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const ReqDev& R,
                                            const DualStats<L>& D, int64_t r, int64_t col, int64_t o,
                                            int64_t lin) {
     double score = 0.0;
@@ -644,9 +644,9 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, const ReqDev& 
             for (int j = i; j < L; ++j) a[i][j] = D.c_out[i][j];
         double delta = 0.0;
         const int code = chol_quad<L>(a, D.md, R.ridge, score, delta);
-        if (lin == P.diag_lin) *P.diag_out = delta;
+        if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
-            report(P, r, col, code);
+            report(P, q, r, col, code);
             score = 0.0;
         }
     }
@@ -735,7 +735,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
 #pragma unroll
             for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
             add_moments<L>(bg, yc, -1.0);
-            lrx_solve<L>(P, R, bg, R.n_a, ZC && cnt[0] - nzc == 0, nzc, yc, r, col, o, lin);
+            lrx_solve<L>(P, q, R, bg, R.n_a, ZC && cnt[0] - nzc == 0, nzc, yc, r, col, o, lin);
         }
 #ifdef HSAD_PHASE_TIMERS
         long long q0 = clock64();  // phases 5/6 sampled on thread 0 of each CTA (x128)
@@ -745,7 +745,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                 DualStats<L> D;
                 dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, ZC && cnt[1] == 0, ZC && cnt[0] - cnt[1] == 0, D);
                 for (int q = 0; q < P.nreq; ++q)  // DWRX first: C_ann dies before the eigensolve
-                    if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L>(P, s_req[q], D, r, col, o, lin);
+                    if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L>(P, q, s_req[q], D, r, col, o, lin);
 #ifdef HSAD_PHASE_TIMERS
                 long long q1 = clock64();
                 if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[5], 128ull * (q1 - q0));
@@ -776,7 +776,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                     for (int c = 0; c < NC; ++c) bg[c] -= g[c];
                     nz_bg -= select_cnt<NBOX>(cnt, R.box_b);
                 }
-                lrx_solve<L>(P, R, bg, R.n_a, ZC && nz_bg == 0, nzc, yc, r, col, o, lin);
+                lrx_solve<L>(P, q, R, bg, R.n_a, ZC && nz_bg == 0, nzc, yc, r, col, o, lin);
             } else {
                 double s_in[NC], s_box[NC];
                 select_box<L, NBOX>(S, R.box_b, s_in);
@@ -785,7 +785,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                 const int nz_box = select_cnt<NBOX>(cnt, R.box_a);
                 DualStats<L> D;
                 dual_stats<L>(s_in, s_box, R.n_a, R.n_b, ZC && nz_in == 0, ZC && nz_box - nz_in == 0, D);
-                if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, R, D, r, col, o, lin);
+                if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, q, R, D, r, col, o, lin);
                 else dwest_solve<L>(R, D, o);
             }
         }
@@ -1146,22 +1146,6 @@ cudaError_t launch_bands(int bands, const DetectParams& P, dim3 grid, int nt, in
     return cudaErrorInvalidValue;
 }
 
-// Stream-ordered scratch (flags, status words) comes from the device's default memory
-// pool; with the default release threshold (0) the pool returns its memory at every
-// synchronisation and the next cudaMallocAsync maps pages again (measured: ~10 ms
-// stalls). Keep the pool's memory once per process and device.
-void keep_pool_memory() {
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    done_dev = dev;
-}
-
 // The staged (standard-layout fp64) kernel runs as a fast pass plus a counting pass
 // that recomputes only the CTAs which met an all-zero spectrum; their per-CTA flags
 // live in a stream-ordered scratch allocation.
@@ -1171,15 +1155,14 @@ cudaError_t launch_detect(int bands, const DetectParams& P0, dim3 grid, int nt, 
     P.zflag = nullptr;
     unsigned char* flags = nullptr;
     if (P.staged) {
-        keep_pool_memory();
         const size_t n = static_cast<size_t>(grid.x) * grid.y;
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flags), n, s);
+        cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&flags), n, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, n, s);
         if (e != cudaSuccess) return e;
         P.zflag = flags;
     }
     const cudaError_t e = launch_bands(bands, P, grid, nt, kcols, s);
-    if (flags) cudaFreeAsync(flags, s);
+    if (flags) scratch_free(flags, s);
     return e;
 }
 
@@ -1314,7 +1297,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                               int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
                               int64_t row_begin, int64_t row_end,
                               const hsad_detect_request* requests, int32_t n_requests,
-                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s) {
+                              int req_base, uint64_t* d_status, hsad_pixel_error* err,
+                              cudaStream_t s) {
     if (err) {
         err->code = HSAD_OK;
         err->row = err->col = -1;
@@ -1405,7 +1389,9 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                smem_for(kc) + static_cast<int64_t>(stage_bytes(P.nbox, P.tw + 2 * P.rmax, bands)) <=
                    smem_cap &&
                !getenv("HSAD_NO_STAGE");
+    P.req_base = req_base;
     P.diag_lin = -1;
+    P.diag_req = -1;
     P.diag_out = nullptr;
     const int64_t strips = (samples + P.tw - 1) / P.tw;
     const int64_t chunks = (row_end - row_begin + P.chunk - 1) / P.chunk;
@@ -1414,17 +1400,19 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
 
     const bool sync = d_status == nullptr;
     unsigned long long* status = reinterpret_cast<unsigned long long*>(d_status);
+    ScratchGuard status_guard(s);  // frees the internal status word on every return path
     if (sync) {
         // the caller-owned d_status accumulates (atomicMin) across calls; the
         // internal one is reset here
-        HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), 2 * sizeof(double), s));
+        HSAD_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&status), 2 * sizeof(double), s));
+        status_guard.p = status;
         HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     }
     P.status = status;
     // diagnostic scratch per request: scores (8 B/px) + eigen-count (1 B/px), 16-byte aligned
     const size_t scratch_stride = (static_cast<size_t>(samples) * 9 + 15) / 16 * 16;
     // full-band launcher: one fullband_kernel launch per request over rows [rb, re)
-    auto launch_fb = [&](int64_t rb, int64_t re, int64_t diag_lin, double* diag_out,
+    auto launch_fb = [&](int64_t rb, int64_t re, int64_t diag_lin, int diag_req, double* diag_out,
                          char* scratch) -> hsad_status {
         for (int q = 0; q < n_requests; ++q) {
             const hsad_detect_request& R = requests[q];
@@ -1445,7 +1433,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                                : R.d_scores;
             F.score_bytes = R.score_bytes;
             F.status = status;
-            F.diag_lin = diag_lin;
+            F.req = req_base + q;
+            F.diag_lin = req_base + q == diag_req ? diag_lin : -1;
             F.diag_out = diag_out;
             hsad_status fst = fullband_launch(F, s);
             if (fst != HSAD_OK) return fst;
@@ -1454,7 +1443,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     };
     cudaError_t e = cudaSuccess;
     if (fullband) {
-        hsad_status fst = launch_fb(row_begin, row_end, -1, nullptr, nullptr);
+        hsad_status fst = launch_fb(row_begin, row_end, -1, -1, nullptr, nullptr);
         if (fst != HSAD_OK) return fst;
     } else {
         e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
@@ -1467,9 +1456,10 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     HSAD_CUDA_TRY(cudaStreamSynchronize(s));
     hsad_status result = HSAD_OK;
     if (packed != ~0ull) {
-        const int code = static_cast<int>(packed & 0x7f);
+        const int code = failure_code(packed);
         const bool overflow = (packed & kCodeOverflow) != 0;
-        const int64_t lin = static_cast<int64_t>(packed >> 8);
+        const int64_t lin = failure_pixel(packed);
+        const int fail_req = failure_request(packed);
         const int64_t row = lin / samples, col = lin % samples;
         std::string msg;
         if (overflow) {
@@ -1482,12 +1472,13 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             D.row_begin = row;
             D.row_end = row + 1;
             D.diag_lin = lin;
+            D.diag_req = fail_req;
             D.diag_out = d_diag;
             // the diagnostic pass writes into scratch rows, never over the results
             char* scratch = nullptr;
-            e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                scratch_stride * D.nreq, s);
+            e = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_stride * D.nreq, s);
             if (e != cudaSuccess) return cuda_fail(e, "hsad detect diagnostics");
+            ScratchGuard scratch_guard(s, scratch);
             for (int q = 0; q < D.nreq; ++q) {
                 D.req[q].scores = scratch + scratch_stride * q;
                 if (D.req[q].eigcount)
@@ -1495,14 +1486,13 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                         scratch + scratch_stride * q + static_cast<size_t>(samples) * 8);
             }
             if (fullband) {
-                if (launch_fb(row, row + 1, lin, d_diag, scratch) != HSAD_OK) e = cudaErrorUnknown;
+                if (launch_fb(row, row + 1, lin, fail_req, d_diag, scratch) != HSAD_OK) e = cudaErrorUnknown;
             } else {
                 e = launch_detect(bands, D, dim3(plan.grid.x, 1), plan.nt, plan.kcols, s);
             }
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(&delta, d_diag, sizeof(double), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-            cudaFreeAsync(scratch, s);
             if (e != cudaSuccess) return cuda_fail(e, "hsad detect diagnostics");
             msg = "covariance numerically singular (ridge " + std::to_string(delta) + ")";
         }
@@ -1515,7 +1505,6 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             err->col = col;
         }
     }
-    cudaFreeAsync(status, s);
     return result;
 }
 
@@ -1576,7 +1565,7 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             ++g1;
         }
         hsad_status st = detect_group_impl(d_cube, elem_bytes, lines, samples, bands, buf_row0,
-                                           buf_rows, row_begin, row_end, requests + g0, g1 - g0,
+                                           buf_rows, row_begin, row_end, requests + g0, g1 - g0, g0,
                                            d_status, err, s);
         if (st != HSAD_OK) return st;
         g0 = g1;

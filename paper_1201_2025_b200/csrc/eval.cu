@@ -415,12 +415,12 @@ struct Scratch {
     template <typename T>
     T* get(size_t count) {
         void* p = nullptr;
-        if (cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), s) != cudaSuccess) return nullptr;
+        if (scratch_alloc(&p, std::max<size_t>(count, 1) * sizeof(T), s) != cudaSuccess) return nullptr;
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     ~Scratch() {
-        for (void* p : ptrs) cudaFreeAsync(p, s);
+        for (void* p : ptrs) scratch_free(p, s);
     }
 };
 

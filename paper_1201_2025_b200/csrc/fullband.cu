@@ -324,14 +324,11 @@ __global__ void __launch_bounds__(kFbThreads, 1) fullband_kernel(const FbParams 
         if (t == 0) {
             const bool singular = s_bad || !(s_dmax > 0.0) || s_dmin <= s_dmax * 1e-14;
             if (singular) {
-                const unsigned long long packedc =
-                    (static_cast<unsigned long long>(lin) << 8) | HSAD_E_SINGULAR_AFTER_RIDGE;
-                atomicMin(P.status, packedc);
+                atomicMin(P.status, pack_failure(P.req, lin, HSAD_E_SINGULAR_AFTER_RIDGE));
             } else {
                 score = -s_piv;  // Schur complement: 0 - d^T (C + delta I)^-1 d
                 if (!isfinite(score)) {
-                    atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
-                                            (HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
+                    atomicMin(P.status, pack_failure(P.req, lin, HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
                     score = 0.0;
                 }
             }
@@ -675,13 +672,11 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
         if (t == 0) {
             const bool singular = s_bad || !(s_dmax > 0.0) || s_dmin <= s_dmax * 1e-14;
             if (singular) {
-                atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
-                                        HSAD_E_SINGULAR_AFTER_RIDGE);
+                atomicMin(P.status, pack_failure(P.req, lin, HSAD_E_SINGULAR_AFTER_RIDGE));
             } else {
                 score = -s_corner[L & 7];
                 if (!isfinite(score)) {
-                    atomicMin(P.status, (static_cast<unsigned long long>(lin) << 8) |
-                                            (HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
+                    atomicMin(P.status, pack_failure(P.req, lin, HSAD_E_SINGULAR_AFTER_RIDGE | 0x80));
                     score = 0.0;
                 }
             }

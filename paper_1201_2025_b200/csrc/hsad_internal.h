@@ -18,6 +18,23 @@ const char* status_name(int32_t code);
 // Maps a CUDA runtime failure to HSAD_E_CUDA with the CUDA error text.
 hsad_status cuda_fail(cudaError_t e, const char* what);
 
+// Stream-ordered scratch (status words, flags, temporaries) comes from a memory pool
+// the library owns per device (release threshold: keep), so repeated calls do not
+// remap pages and the process's default pool is left untouched (api.cu).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+void scratch_free(void* p, cudaStream_t s);
+// Frees one scratch allocation on every return path.
+struct ScratchGuard {
+    cudaStream_t s;
+    void* p;
+    explicit ScratchGuard(cudaStream_t st, void* q = nullptr) : s(st), p(q) {}
+    ScratchGuard(const ScratchGuard&) = delete;
+    ScratchGuard& operator=(const ScratchGuard&) = delete;
+    ~ScratchGuard() {
+        if (p) scratch_free(p, s);
+    }
+};
+
 #define HSAD_CUDA_TRY(expr)                                              \
     do {                                                                 \
         cudaError_t e__ = (expr);                                        \
@@ -105,11 +122,27 @@ struct FbParams {
     void* scores;
     int score_bytes;
     unsigned long long* status;
+    int req;            // position of the request in the call (failure ordering)
     int64_t diag_lin;
     double* diag_out;
     int chunk;          // samples per shared-memory chunk (set by fullband_launch)
     int mp;             // bordered dimension L+1 rounded up to a multiple of 4
 };
+
+// Packed per-pixel failure word (atomicMin across a call): the request's position in
+// the call's request list in bits 56..63, the pixel (row*samples + col) in bits 8..55,
+// the hsad_status code in bits 0..6 (bit 7: the "inverse overflowed" variant). The
+// minimum is the first failing pixel of the first failing request: what the equivalent
+// sequential hsad::detect calls report (detect.cpp:127-130, parallel.hpp:17-40).
+constexpr unsigned long long kFailPixelMask = (1ull << 48) - 1;
+__host__ __device__ inline unsigned long long pack_failure(int req, int64_t lin, int code) {
+    return (static_cast<unsigned long long>(req) << 56) |
+           ((static_cast<unsigned long long>(lin) & kFailPixelMask) << 8) |
+           static_cast<unsigned long long>(code & 0xff);
+}
+inline int64_t failure_pixel(unsigned long long w) { return static_cast<int64_t>((w >> 8) & kFailPixelMask); }
+inline int failure_request(unsigned long long w) { return static_cast<int>(w >> 56); }
+inline int failure_code(unsigned long long w) { return static_cast<int>(w & 0x7f); }
 
 // Kernel-side limits.
 constexpr int kMaxDetectBands = 8;

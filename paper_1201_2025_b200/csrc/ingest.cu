@@ -424,11 +424,11 @@ extern "C" hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, con
         // BIP: decode (read_cube) into a stream-ordered fp64 cube, then the TMA DWT
         void* tmp = nullptr;
         const size_t n = static_cast<size_t>(h.lines) * h.samples * h.bands;
-        HSAD_CUDA_TRY(cudaMallocAsync(&tmp, n * sizeof(double), s));
+        HSAD_CUDA_TRY(scratch_alloc(&tmp, n * sizeof(double), s));
+        ScratchGuard tmp_guard(s, tmp);
         st = hsad_read_cube(d_raw, raw_bytes, &h, tmp, 8, stream);
         if (st == HSAD_OK)
             st = hsad_reduce(tmp, 8, h.lines, h.samples, h.bands, order, target_bands, d_out, out_bytes, stream);
-        cudaFreeAsync(tmp, s);
         return st;
     }
     if (target_bands != 1 && target_bands != 2 && target_bands != 4 && target_bands != 8 &&
@@ -438,13 +438,13 @@ extern "C" hsad_status hsad_reduce_raw(const void* d_raw, int64_t raw_bytes, con
     st = device_wavelet_map(h.bands, order, target_bands, &d_map);  // plan errors before any launch
     if (st != HSAD_OK) return st;
     unsigned long long* status = nullptr;
-    HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
+    HSAD_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
+    ScratchGuard status_guard(s, status);
     HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     cudaError_t e = reduce_raw_rows(h, d_raw, order, target_bands, d_out, out_bytes, status, s, 0, h.lines);
     unsigned long long first = ~0ull;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&first, status, sizeof(first), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFreeAsync(status, s);
     if (e != cudaSuccess) return cuda_fail(e, "hsad_reduce_raw");
     if (first != ~0ull) return nonfinite_error(h, first);
     return HSAD_OK;
@@ -466,14 +466,14 @@ extern "C" hsad_status hsad_read_cube(const void* d_raw, int64_t raw_bytes, cons
     // every supported host is little-endian: swap when the file is big-endian (cube.cpp:205)
     const bool swap = h.byte_order == 1;
     unsigned long long* status = nullptr;
-    HSAD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
+    HSAD_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
+    ScratchGuard status_guard(s, status);
     HSAD_CUDA_TRY(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     cudaError_t e = out_bytes == 8 ? dispatch_code<double>(h, d_raw, swap, d_out, status, s)
                                    : dispatch_code<float>(h, d_raw, swap, d_out, status, s);
     unsigned long long first = ~0ull;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&first, status, sizeof(first), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFreeAsync(status, s);
     if (e != cudaSuccess) return cuda_fail(e, "hsad_read_cube");
     if (first != ~0ull) return nonfinite_error(h, first);  // cube.cpp:244-247
     return HSAD_OK;

@@ -221,7 +221,7 @@ extern "C" hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, in
     if (packed == ~0ull) return HSAD_OK;
     // a pixel failed: re-run its row chunk synchronously for the reference message
     // (identical arithmetic: same rows resident, chunk-aligned range)
-    const int64_t row = static_cast<int64_t>(packed >> 8) / samples;
+    const int64_t row = failure_pixel(packed) / samples;
     const int64_t a = row / quantum * quantum;
     const int64_t b = a + quantum < lines ? a + quantum : lines;
     hsad_detect_request part[kMaxCallRequests];
@@ -375,7 +375,7 @@ extern "C" hsad_status hsad_pipeline_raw(const void* h_raw, int64_t raw_bytes, c
     if (words[1] != ~0ull) return nonfinite_error(h, words[1]);  // read_cube fails first
     if (words[0] == ~0ull) return HSAD_OK;
     // a pixel failed: its row chunk again, synchronously, for the reference message
-    const int64_t row = static_cast<int64_t>(words[0] >> 8) / samples;
+    const int64_t row = failure_pixel(words[0]) / samples;
     const int64_t a = row / quantum * quantum;
     const int64_t b = a + quantum < lines ? a + quantum : lines;
     hsad_detect_request part[kMaxCallRequests];

@@ -236,8 +236,28 @@ cudaError_t launch_tb(const Tin* cube, int64_t npix, int bands, const double* wm
                       int out_bytes, cudaStream_t s) {
     constexpr int G = 32 / TARGET;
     const int tile = bulk_tile_px(bands, sizeof(Tin));
+    // cp.async.bulk needs a 16-byte aligned source: a cube (or a row strip of one) whose
+    // base is not, starts the bulk path at the first pixel that is, and the lane-split
+    // kernel (same arithmetic, bit-identical) takes the leading pixels
+    int64_t lead = -1;
+    const uintptr_t pix_bytes = static_cast<uintptr_t>(bands) * sizeof(Tin);
+    for (int64_t p = 0; p < 16 && p < npix; ++p)
+        if ((reinterpret_cast<uintptr_t>(cube) + p * pix_bytes) % 16 == 0) {
+            lead = p;
+            break;
+        }
+    if (lead > 0) {
+        const int grid = grid_for((lead + G - 1) / G, kWarps);
+        reduce_lanesplit_kernel<Tin, TARGET, B><<<grid, kWarps * 32, 0, s>>>(
+            cube, lead, bands, wmap, out, out_bytes);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        cube += lead * bands;
+        out = static_cast<char*>(out) + lead * TARGET * out_bytes;
+        npix -= lead;
+    }
     int64_t done = 0;
-    if (tile > 0 && npix >= tile) {
+    if (lead >= 0 && tile > 0 && npix >= tile) {
         const int64_t tiles = npix / tile;
         const size_t smem = 128 + static_cast<size_t>(kStages) * tile * bands * sizeof(Tin);
         auto k = reduce_bulk_kernel<Tin, TARGET, B>;

@@ -86,10 +86,17 @@ def test_strip_rows_and_quantum():
 
 
 def test_decode_status():
+    """Failure word: request position (bits 56..63), pixel (8..55), code (0..6) with
+    the 0x80 "inverse overflowed" flag masked off."""
     lib = _abi.lib()
     e = _abi.PixelError()
     assert lib.hsad_decode_status((((7 * 100 + 3) << 8) | 13), 100, C.byref(e)) == 13
     assert (e.code, e.row, e.col) == (13, 7, 3)
+    assert lib.hsad_decode_status((((7 * 100 + 3) << 8) | 13 | 0x80), 100, C.byref(e)) == 13
+    assert (e.code, e.row, e.col) == (13, 7, 3)
+    word = (5 << 56) | ((4095 * 4096 + 17) << 8) | 13
+    assert lib.hsad_decode_status(word, 4096, C.byref(e)) == 13
+    assert (e.code, e.row, e.col) == (13, 4095, 17)
     assert lib.hsad_decode_status(2**64 - 1, 100, C.byref(e)) == 0
 
 

@@ -1,0 +1,159 @@
+"""GPU edge cases: misaligned strips into the TMA reduction, failure ordering inside a
+fused launch, and the fp32 score path on the BASELINE configs.
+
+* cp.async.bulk needs a 16-byte aligned source; row strips of an odd-samples x
+  odd-bands fp32 cube (bands = 189 is the paper's count) start 4 or 8 bytes off.
+* A fused group of requests must report what the equivalent sequential hsad::detect
+  calls report: the first failing request (in request order), at its first failing
+  pixel in row-major order (detect.cpp:127-130, parallel.hpp:17-40).
+* The fp32 path (score_bytes = 4) stores fp32 maps of the same fp64 arithmetic:
+  within 1e-4 (rel_diff, proj/tests/support/testutil.hpp:34-36) of the fp64 oracle,
+  with identical top-k sets and DWEST eigen-counts (BASELINE north star).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import OracleError, max_rel_diff  # noqa: E402
+
+hs = pytest.importorskip("paper_1201_2025_b200")
+from harness.scene import CONFIGS, generate_scene  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def W1(n):
+    return hs.WindowConfig.single(n)
+
+
+def W2(i, o):
+    return hs.WindowConfig.dual(i, o)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_reduce_misaligned_row_views(orc, dtype):
+    cube = orc.port.random_cube(40, 101, 189, 77).astype(dtype)
+    g = torch.as_tensor(cube).to(DEV)
+    whole = hs.reduce_cube(g, 2, 4)
+    for r in (1, 3, 7):
+        view = g[r:]
+        assert view.data_ptr() % 16 != 0
+        part = hs.reduce_cube(view, 2, 4)
+        assert torch.equal(part, whole[r:])  # leading pixels through the lane-split kernel
+        assert max_rel_diff(part.cpu().numpy(), orc.port.reduce_cube(cube[r:], 2, 4)) < 1e-12
+
+
+def test_pipeline_host_odd_samples_odd_bands_many_strips(orc):
+    # 1000 x 101 x 189 fp32 = 76 MB: several row strips, each starting off 16-byte alignment
+    cube = torch.as_tensor(orc.port.random_cube(1000, 101, 189, 78).astype(np.float32))
+    h = cube.pin_memory()
+    reqs = [hs.DetectRequest("lrx", W1(11)), hs.DetectRequest("dwest", W2(5, 11), eigcount=True)]
+    outs = [(torch.empty((1000, 101), dtype=torch.float64).pin_memory(),
+             torch.empty((1000, 101), dtype=torch.int8) if r.eigcount else None) for r in reqs]
+    hs.pipeline_host(h, 2, 4, reqs, outs)
+    dev = hs.detect_multi(hs.reduce_cube(cube.to(DEV), 2, 4), reqs)
+    for (a, ac), (b, bc) in zip(outs, dev):
+        assert torch.equal(a, b.cpu())
+        if ac is not None:
+            assert torch.equal(ac, bc.cpu())
+
+
+def _two_failure_cube(orc):
+    """LRX 3 (ridge 0) first fails at (5, 5); DWRX 1/5 (ridge 0) first fails later."""
+    cube = orc.port.random_cube(20, 20, 4, 79)
+    cube[4:7, 4:7] = 0.25          # constant 3x3 background around (5, 5) ...
+    cube[5, 5] = (1.0, 0.0, 0.5, 0.0)  # ... with a different centre
+    cube[10:15, 10:15] = 0.75      # constant 5x5 annulus around (12, 12) ...
+    cube[12, 12] = (0.0, 1.0, 0.0, 0.5)
+    return cube
+
+
+def test_fused_group_reports_first_failing_request(orc):
+    cube = _two_failure_cube(orc)
+    with pytest.raises(OracleError) as e_dwrx:
+        orc.port.dwrx(cube, 1, 5, 0.0)
+    with pytest.raises(OracleError) as e_lrx:
+        orc.port.local_rx(cube, 3, 0.0)
+    p_dwrx = (e_dwrx.value.row, e_dwrx.value.col)
+    p_lrx = (e_lrx.value.row, e_lrx.value.col)
+    assert p_lrx < p_dwrx  # the later request fails at the earlier pixel
+    g = torch.as_tensor(cube).to(DEV)
+    # different outer windows: two launches, the first group's failure wins
+    reqs = [hs.DetectRequest("dwrx", W2(1, 5), ridge=0.0), hs.DetectRequest("lrx", W1(3), ridge=0.0)]
+    with pytest.raises(hs.HsadError) as got:
+        hs.detect_multi(g, reqs)
+    assert (got.value.row, got.value.col) == p_dwrx
+    assert str(got.value) == str(e_dwrx.value)
+    # reversed order: LRX is the first request, so its pixel is reported
+    with pytest.raises(hs.HsadError) as got2:
+        hs.detect_multi(g, reqs[::-1])
+    assert (got2.value.row, got2.value.col) == p_lrx
+    assert str(got2.value) == str(e_lrx.value)
+
+
+def test_fused_group_same_window_failure_order(orc):
+    """LRX and DWRX sharing the outer window run in ONE fused launch; the failure word
+    carries the request position, so the first failing request wins over a lower pixel."""
+    cube = orc.port.random_cube(24, 24, 4, 80)
+    cube[14:19, 14:19] = 0.5
+    cube[16, 16] = (1.0, 0.0, 0.0, 0.0)   # DWRX 1/5 annulus constant at (16, 16)
+    cube[2:7, 2:7] = 0.125                 # LRX 5: constant background around (4, 4)
+    cube[4, 4] = (0.0, 0.0, 1.0, 0.0)
+    want = {}
+    for name, fn in (("dwrx", lambda: orc.port.dwrx(cube, 1, 5, 0.0)),
+                     ("lrx", lambda: orc.port.local_rx(cube, 5, 0.0))):
+        with pytest.raises(OracleError) as e:
+            fn()
+        want[name] = e.value
+    assert (want["lrx"].row, want["lrx"].col) < (want["dwrx"].row, want["dwrx"].col)
+    g = torch.as_tensor(cube).to(DEV)
+    reqs = [hs.DetectRequest("dwrx", W2(1, 5), ridge=0.0), hs.DetectRequest("lrx", W1(5), ridge=0.0)]
+    with pytest.raises(hs.HsadError) as got:
+        hs.detect_multi(g, reqs)
+    assert str(got.value) == str(want["dwrx"])
+    # asynchronous status word: same ordering, decoded by hsad_decode_status
+    st = torch.full((1,), -1, dtype=torch.int64, device=DEV)
+    hs.detect_multi(g, reqs, status=st)
+    torch.cuda.synchronize()
+    word = int(st.item()) & (2**64 - 1)
+    assert word >> 56 == 0  # request 0 (DWRX)
+    e = hs._abi.PixelError()
+    import ctypes as C
+    assert hs._abi.lib().hsad_decode_status(word, 24, C.byref(e)) == 13
+    assert (e.row, e.col) == (want["dwrx"].row, want["dwrx"].col)
+
+
+@pytest.mark.parametrize("name,spec", [
+    ("C1", [("lrx", (9,), {"guard": 3}), ("lrx", (9,), {})]),
+    ("C2", [("dwrx", (5, 11), {}), ("dwest", (5, 11), {})]),
+    ("C4", [("lrx", (11,), {}), ("dwrx", (5, 11), {}), ("dwest", (5, 11), {})]),
+])
+def test_fp32_path_on_configs(orc, name, spec):
+    cfg = CONFIGS[name]
+    cube, truth = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"],
+                                 cfg["rate"], device=DEV)
+    red = hs.reduce_cube(cube, 2, 4)
+    red_o = orc.port.reduce_cube(cube.cpu().numpy(), 2, 4, workers=8)
+    reqs = []
+    for a, w, kw in spec:
+        win = W1(*w) if a == "lrx" else W2(*w)
+        reqs.append(hs.DetectRequest(a, win, eigcount=(a == "dwest"), score_dtype=torch.float32, **kw))
+    outs = hs.detect_multi(red, reqs)
+    torch.cuda.synchronize()
+    k = int(truth.sum())
+    for (a, w, kw), (s, c) in zip(spec, outs):
+        assert s.dtype == torch.float32
+        s = s.cpu().numpy().astype(np.float64)
+        if a == "lrx":
+            want = orc.port.local_rx(red_o, w[0], 1e-6, guard=kw.get("guard", 1), workers=8)
+        elif a == "dwrx":
+            want = orc.port.dwrx(red_o, w[0], w[1], 1e-6, workers=8)
+        else:
+            want, wc = orc.port.dwest(red_o, w[0], w[1], 0.1, workers=8)
+            assert np.array_equal(c.cpu().numpy(), wc), f"{name} {a} eigen-counts"
+        assert max_rel_diff(s, want) < 1e-4, f"{name} {a}"
+        top_g = set(np.argsort(-s.ravel(), kind="stable")[:k].tolist())
+        top_o = set(np.argsort(-want.ravel(), kind="stable")[:k].tolist())
+        assert top_g == top_o, f"{name} {a} top-{k}"
