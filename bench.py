@@ -304,7 +304,7 @@ def run_reference(args, cfg, rank, world):
     import oracle
     cores = os.cpu_count() or 1
     lines, samples, bands = cfg["lines"], cfg["samples"], cfg["bands"]
-    half = 8
+    half = 32
     mid = lines // 2
     bands_rows = [(0, half), (mid, mid + half)]  # border rows and interior rows
     cubes = []

@@ -55,7 +55,12 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s);
 
 namespace {
 
-constexpr int kCodeOverflow = 0x80;  // flag: "inverse overflowed" variant of SingularAfterRidge
+constexpr int kCodeOverflow = 0x80;
+// Boxes of at least this radius use the lane-pair horizontal sums (K = 1 kernels)
+#ifndef HSAD_PAIR_RADIUS
+#define HSAD_PAIR_RADIUS 2
+#endif
+constexpr int kPairRadius = HSAD_PAIR_RADIUS;  // flag: "inverse overflowed" variant of SingularAfterRidge
 
 struct ReqDev {
     int algo;         // hsad_algorithm
@@ -1006,7 +1011,9 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
             if (t == 0 && r > ra && r + 1 < rb) issue_rows(r + 1);  // ra + 1: issued at start
         }
         PT_MARK(1);  // barrier A
-        if (seg0 < P.tw && c0 + seg0 < P.samples) {
+        // K = 1: every lane forms its horizontal sums (the lane pairs exchange halves
+        // with shuffles), then lanes outside the image skip the solves
+        if (K == 1 || (seg0 < P.tw && c0 + seg0 < P.samples)) {
             double S[NBOX][NC];
             int cnt[NBOX];
             // horizontal window of the first column of the segment
@@ -1016,14 +1023,54 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
                 for (int i = 0; i < NC; ++i) S[k][i] = 0.0;
                 const int R = P.radius[k];
                 int ck = 0;
-                for (int d = -R; d <= R; ++d) {
-                    if constexpr (ZC) ck += s_nz[k * ncol + P.rmax + seg0 + d];
-                    const double2* src = vslot(k, P.rmax + seg0 + d);
+                if constexpr (ZC) {
+                    for (int d = -R; d <= R; ++d) ck += s_nz[k * ncol + P.rmax + seg0 + d];
+                }
+                if (K == 1 && R >= kPairRadius) {
+                    // Lane pair (even column c, odd column c + 1): the windows share the
+                    // 2R columns [c + 1 - R, c + R]. The even lane sums [c + 1 - R, c]
+                    // (walking down from c), the odd lane [c + 1, c + R] (walking up),
+                    // they swap halves, and each adds its own edge column (c - R or
+                    // c + 1 + R): R + 1 column reads per box instead of 2R + 1, and the
+                    // opposite walking directions keep the LDS.128 conflict-free. The
+                    // core is (lower half + upper half) in both lanes, so each pixel's
+                    // summation order depends only on its global column parity.
+                    const bool odd = (t & 1) != 0;
+                    const int own = P.rmax + seg0;
+                    double h[NC];
+#pragma unroll
+                    for (int i = 0; i < NC; ++i) h[i] = 0.0;
+                    for (int d = 0; d < R; ++d) {
+                        const double2* src = vslot(k, odd ? own + d : own - d);
+#pragma unroll
+                        for (int c2 = 0; c2 < NC2; ++c2) {
+                            const double2 v = src[c2];
+                            h[2 * c2] += v.x;
+                            if (2 * c2 + 1 < NC) h[2 * c2 + 1] += v.y;
+                        }
+                    }
+                    const double2* e = vslot(k, odd ? own + R : own - R);
 #pragma unroll
                     for (int c2 = 0; c2 < NC2; ++c2) {
-                        const double2 v = src[c2];
-                        S[k][2 * c2] += v.x;
-                        if (2 * c2 + 1 < NC) S[k][2 * c2 + 1] += v.y;
+                        const double2 v = e[c2];
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int i = 2 * c2 + hh;
+                            if (i >= NC) break;
+                            const double other = __shfl_xor_sync(0xffffffffu, h[i], 1);
+                            const double core = odd ? other + h[i] : h[i] + other;
+                            S[k][i] = core + (hh == 0 ? v.x : v.y);
+                        }
+                    }
+                } else {
+                    for (int d = -R; d <= R; ++d) {
+                        const double2* src = vslot(k, P.rmax + seg0 + d);
+#pragma unroll
+                        for (int c2 = 0; c2 < NC2; ++c2) {
+                            const double2 v = src[c2];
+                            S[k][2 * c2] += v.x;
+                            if (2 * c2 + 1 < NC) S[k][2 * c2 + 1] += v.y;
+                        }
                     }
                 }
                 cnt[k] = ck;
@@ -1494,7 +1541,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                 e = cudaMemcpyAsync(&delta, d_diag, sizeof(double), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) return cuda_fail(e, "hsad detect diagnostics");
-            msg = "covariance numerically singular (ridge " + std::to_string(delta) + ")";
+            // -0.0 (ridge 0 times a rounding-negative trace) prints as the reference's 0
+            msg = "covariance numerically singular (ridge " + std::to_string(delta + 0.0) + ")";
         }
         result = static_cast<hsad_status>(code);
         set_error(result, std::string(status_name(code)) + ": " + msg + " at pixel (" +
