@@ -93,36 +93,63 @@ def test_fused_group_reports_first_failing_request(orc):
     assert str(got2.value) == str(e_lrx.value)
 
 
+def _same_window_cube():
+    """Integer-valued 24 x 24 x 4 cube (exact sums): LRX 5 (ridge 0) first fails at (4, 4),
+    DWRX 3/5 (ridge 0) first fails later, at (16, 16).
+
+    Around (4, 4) the 5x5 box lies in the plane a + t e1 + s e2 (rank-2 background:
+    LRX singular, centre off the background mean), while the inner 3x3 mean equals the
+    annulus mean exactly (DWRX scores 0 without a solve). Around (16, 16) the annulus
+    is constant and the centre differs (DWRX singular)."""
+    rng = np.random.default_rng(81)
+    cube = rng.integers(0, 8, (24, 24, 4)).astype(np.float64)
+    a = np.array([2.0, 2.0, 2.0, 2.0])
+    e1 = np.array([1.0, 0, 0, 0]); e2 = np.array([0, 1.0, 0, 0])
+    t_ann = iter([1, -1] * 8)
+    t_in = iter([1, -1, 1, -1, 1, -1, 1, -1])
+    for dr in range(-2, 3):
+        for dc in range(-2, 3):
+            if max(abs(dr), abs(dc)) == 2:
+                cube[4 + dr, 4 + dc] = a + next(t_ann) * e1
+            elif (dr, dc) != (0, 0):
+                cube[4 + dr, 4 + dc] = a + next(t_in) * e1
+    cube[3, 3] += e2            # one ring pixel off the line ...
+    cube[4, 4] = a - e2         # ... and the centre opposite: inner mean == annulus mean
+    cube[14:19, 14:19] = 5.0
+    cube[16, 16] = (1.0, 3.0, 5.0, 7.0)
+    return cube
+
+
 def test_fused_group_same_window_failure_order(orc):
     """LRX and DWRX sharing the outer window run in ONE fused launch; the failure word
     carries the request position, so the first failing request wins over a lower pixel."""
-    cube = orc.port.random_cube(24, 24, 4, 80)
-    cube[14:19, 14:19] = 0.5
-    cube[16, 16] = (1.0, 0.0, 0.0, 0.0)   # DWRX 1/5 annulus constant at (16, 16)
-    cube[2:7, 2:7] = 0.125                 # LRX 5: constant background around (4, 4)
-    cube[4, 4] = (0.0, 0.0, 1.0, 0.0)
+    cube = _same_window_cube()
     want = {}
-    for name, fn in (("dwrx", lambda: orc.port.dwrx(cube, 1, 5, 0.0)),
+    for name, fn in (("dwrx", lambda: orc.port.dwrx(cube, 3, 5, 0.0)),
                      ("lrx", lambda: orc.port.local_rx(cube, 5, 0.0))):
         with pytest.raises(OracleError) as e:
             fn()
         want[name] = e.value
-    assert (want["lrx"].row, want["lrx"].col) < (want["dwrx"].row, want["dwrx"].col)
+    assert (want["lrx"].row, want["lrx"].col) == (4, 4)
+    assert (want["dwrx"].row, want["dwrx"].col) == (16, 16)
     g = torch.as_tensor(cube).to(DEV)
-    reqs = [hs.DetectRequest("dwrx", W2(1, 5), ridge=0.0), hs.DetectRequest("lrx", W1(5), ridge=0.0)]
+    reqs = [hs.DetectRequest("dwrx", W2(3, 5), ridge=0.0), hs.DetectRequest("lrx", W1(5), ridge=0.0)]
     with pytest.raises(hs.HsadError) as got:
         hs.detect_multi(g, reqs)
     assert str(got.value) == str(want["dwrx"])
+    with pytest.raises(hs.HsadError) as got2:
+        hs.detect_multi(g, reqs[::-1])
+    assert str(got2.value) == str(want["lrx"])
     # asynchronous status word: same ordering, decoded by hsad_decode_status
+    import ctypes as C
     st = torch.full((1,), -1, dtype=torch.int64, device=DEV)
     hs.detect_multi(g, reqs, status=st)
     torch.cuda.synchronize()
     word = int(st.item()) & (2**64 - 1)
     assert word >> 56 == 0  # request 0 (DWRX)
     e = hs._abi.PixelError()
-    import ctypes as C
     assert hs._abi.lib().hsad_decode_status(word, 24, C.byref(e)) == 13
-    assert (e.row, e.col) == (want["dwrx"].row, want["dwrx"].col)
+    assert (e.row, e.col) == (16, 16)
 
 
 @pytest.mark.parametrize("name,spec", [
