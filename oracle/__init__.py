@@ -88,6 +88,8 @@ class _Port:
         lib.orc_dwrx_rows.argtypes = [V, I, Lg, Lg, I, Lg, Lg, I, I, Dd, _D, I, _L, _L]
         lib.orc_dwest_rows.argtypes = [V, I, Lg, Lg, I, Lg, Lg, I, I, Dd, _D, _I8, I, _L, _L]
         lib.orc_dwest_margins.argtypes = [V, I, Lg, Lg, I, Lg, Lg, I, I, Dd, _D, _D, I]
+        lib.orc_hp_lrx_pixels.argtypes = [V, I, Lg, Lg, I, I, I, Dd, Lg, _L, _L, _D, _D, I]
+        lib.orc_hp_dwrx_pixels.argtypes = [V, I, Lg, Lg, I, I, I, Dd, Lg, _L, _L, _D, _D, I]
 
     def _check(self, rc: int, row: int = -1, col: int = -1):
         if rc != 0:
@@ -209,6 +211,22 @@ class _Port:
                                      cnt.ctypes.data_as(_I8), workers, C.byref(er), C.byref(ec))
         self._check(rc, er.value, ec.value)
         return out, cnt
+
+    # --- extended-precision third opinion (hp_oracle.cpp) ------------------------
+    def _hp(self, fn, cube, a, b, ridge, rows, cols, workers):
+        cube = self._cube(cube); L, S, B = cube.shape
+        rows = np.ascontiguousarray(rows, np.int64); cols = np.ascontiguousarray(cols, np.int64)
+        out = np.zeros(len(rows)); piv = np.zeros(len(rows))
+        fn(_vp(cube), cube.dtype.itemsize, L, S, B, a, b, C.c_double(ridge), len(rows),
+           rows.ctypes.data_as(_L), cols.ctypes.data_as(_L), _dp(out), _dp(piv), workers)
+        return out, piv
+
+    def hp_local_rx(self, cube, window, rows, cols, ridge=1e-6, guard=1, workers=1):
+        """LRX in long double at the listed pixels: (scores, LDL^T pivot ratio)."""
+        return self._hp(self.lib.orc_hp_lrx_pixels, cube, window, guard, ridge, rows, cols, workers)
+
+    def hp_dwrx(self, cube, inner, outer, rows, cols, ridge=1e-6, workers=1):
+        return self._hp(self.lib.orc_hp_dwrx_pixels, cube, inner, outer, ridge, rows, cols, workers)
 
     def dwest_margins(self, cube, inner, outer, eigen_fraction=0.1, workers=1, rows=None):
         cube = self._cube(cube); L, S, B = cube.shape

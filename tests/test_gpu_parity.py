@@ -132,40 +132,6 @@ def test_band_counts(orc, bands):
     assert max_rel_diff(e, s) < TOL64 and np.array_equal(n, c)
 
 
-def _mirror(i, n):
-    if n == 1:
-        return np.zeros_like(i)
-    p = 2 * (n - 1)
-    i = np.abs(i) % p
-    return np.where(i < n, i, p - i)
-
-
-def window_kappa(cube, size, exclude, ridge):
-    """Per-pixel condition number of the ridged window covariance (numpy, test only).
-    exclude = edge of the centred box left out (1 = centre only, 0 = none)."""
-    L, S, B = cube.shape
-    h, eh = size // 2, exclude // 2
-    offs = [(dr, dc) for dr in range(-h, h + 1) for dc in range(-h, h + 1)
-            if not (exclude > 0 and abs(dr) <= eh and abs(dc) <= eh)]
-    r = np.arange(L)[:, None]; c = np.arange(S)[None, :]
-    smp = np.stack([cube[_mirror(r + dr, L), _mirror(c + dc, S)] for dr, dc in offs], axis=2)
-    x = smp - smp.mean(axis=2, keepdims=True)
-    cov = np.einsum("rsni,rsnj->rsij", x, x) / len(offs)
-    tr = np.trace(cov, axis1=2, axis2=3)
-    cov = cov + (ridge * tr / B)[..., None, None] * np.eye(B)
-    return np.linalg.cond(cov)
-
-
-def assert_kappa_close(got, want, kappa, what):
-    """1e-9 (north-star fp64 bar) where the window covariance is well conditioned;
-    for sample-starved windows the bar scales with kappa (backward-stable solvers on
-    both sides differ by ~kappa * eps)."""
-    tol = np.maximum(TOL64, 1e-14 * kappa)
-    err = np.abs(got - want) / np.maximum(1.0, np.maximum(np.abs(got), np.abs(want)))
-    bad = err > tol
-    assert not bad.any(), f"{what}: {int(bad.sum())} px, worst err {err.max():.3g}"
-
-
 @pytest.mark.parametrize("window,inner,outer", [(3, 1, 3), (7, 3, 9), (11, 5, 11), (15, 5, 15),
                                                 (21, 7, 21), (25, 3, 25)])
 def test_window_sizes_and_borders(orc, window, inner, outer):
@@ -174,10 +140,11 @@ def test_window_sizes_and_borders(orc, window, inner, outer):
         cube = orc.port.random_cube(*shape, 4, window * 7 + shape[0])
         (l, _), (d, _) = run(cube, [hs.DetectRequest("lrx", W1(window)),
                                     hs.DetectRequest("dwrx", W2(inner, outer))])
-        assert_kappa_close(l, orc.port.local_rx(cube, window), window_kappa(cube, window, 1, 1e-6),
-                           f"lrx {window} {shape}")
-        dk = window_kappa(cube, outer, inner, 1e-6)
-        assert_kappa_close(d, orc.port.dwrx(cube, inner, outer), dk, f"dwrx {inner}/{outer} {shape}")
+        assert_plain_bar(l, orc.port.local_rx(cube, window),
+                         lambda r, c: orc.port.hp_local_rx(cube, window, r, c)[0], f"lrx {window} {shape}")
+        assert_plain_bar(d, orc.port.dwrx(cube, inner, outer),
+                         lambda r, c: orc.port.hp_dwrx(cube, inner, outer, r, c)[0],
+                         f"dwrx {inner}/{outer} {shape}")
         if inner > 1:
             (e, n), = run(cube, [hs.DetectRequest("dwest", W2(inner, outer), eigcount=True)])
             s, c = orc.port.dwest(cube, inner, outer)
@@ -342,54 +309,59 @@ def test_golden_vectors_from_reference_code():
 
 
 # ------------------------------------------------------------------ full-band path (K5/K6)
-def _fb_kappa(cube, rows, size, excl, ridge):
-    """Condition numbers of the ridged background covariances of the given rows."""
-    L, S, B = cube.shape
-    h, eh = size // 2, excl // 2
-    offs = [(dr, dc) for dr in range(-h, h + 1) for dc in range(-h, h + 1)
-            if not (excl > 0 and abs(dr) <= eh and abs(dc) <= eh)]
-    out = np.zeros((rows[1] - rows[0], S))
-    for i, r in enumerate(range(*rows)):
-        for c in range(S):
-            X = np.array([cube[_mirror(np.array(r + dr), L), _mirror(np.array(c + dc), S)]
-                          for dr, dc in offs])
-            C = np.cov(X.T, bias=True)
-            C += ridge * np.trace(C) / B * np.eye(B)
-            out[i, c] = np.linalg.cond(C)
-    return out
-
-
 @pytest.mark.parametrize("bands,window,inner,outer", [(12, 7, 3, 7), (30, 9, 3, 9), (61, 11, 5, 11)])
 def test_fullband_random_cubes(orc, bands, window, inner, outer):
     cube = orc.port.random_cube(11, 13, bands, 500 + bands)
     (l, _), (d, _) = run(cube, [hs.DetectRequest("lrx", W1(window)),
                                 hs.DetectRequest("dwrx", W2(inner, outer))])
-    assert_kappa_close(l, orc.port.local_rx(cube, window), _fb_kappa(cube, (0, 11), window, 1, 1e-6),
-                       f"fullband lrx L={bands}")
-    assert_kappa_close(d, orc.port.dwrx(cube, inner, outer),
-                       _fb_kappa(cube, (0, 11), outer, inner, 1e-6), f"fullband dwrx L={bands}")
+    assert_plain_bar(l, orc.port.local_rx(cube, window),
+                     lambda r, c: orc.port.hp_local_rx(cube, window, r, c)[0], f"fullband lrx L={bands}")
+    assert_plain_bar(d, orc.port.dwrx(cube, inner, outer),
+                     lambda r, c: orc.port.hp_dwrx(cube, inner, outer, r, c)[0], f"fullband dwrx L={bands}")
     # guard extension at full band
     (g, _), = run(cube, [hs.DetectRequest("lrx", W1(window), guard=3)])
-    assert_kappa_close(g, orc.port.local_rx(cube, window, guard=3),
-                       _fb_kappa(cube, (0, 11), window, 3, 1e-6), f"fullband lrx guard L={bands}")
+    assert_plain_bar(g, orc.port.local_rx(cube, window, guard=3),
+                     lambda r, c: orc.port.hp_local_rx(cube, window, r, c, guard=3)[0],
+                     f"fullband lrx guard L={bands}")
+
+
+def assert_plain_bar(got, want, hp_at, what):
+    """The north-star fp64 bar, 1e-9 rel_diff, against the fp64 oracle on every pixel.
+    Where the kernel and the fp64 oracle differ by more (two backward-stable fp64 solvers
+    at kappa ~1e6-1e7 may differ by ~kappa * eps), the extended-precision third opinion
+    (oracle/hp_oracle.cpp, long double) decides: the kernel must be within 1e-9 of it and
+    no farther from it than the oracle is."""
+    err = np.abs(got - want) / np.maximum(1.0, np.maximum(np.abs(got), np.abs(want)))
+    bad = np.argwhere(err > TOL64)
+    if len(bad) == 0:
+        return 0
+    truth = hp_at(bad[:, 0], bad[:, 1])
+    g, w = got[bad[:, 0], bad[:, 1]], want[bad[:, 0], bad[:, 1]]
+    e_k = np.abs(g - truth) / np.maximum(1.0, np.maximum(np.abs(g), np.abs(truth)))
+    e_o = np.abs(w - truth) / np.maximum(1.0, np.maximum(np.abs(w), np.abs(truth)))
+    assert np.all(e_k <= TOL64), f"{what}: kernel off the long-double value by {e_k.max():.3g}"
+    assert np.all(e_k <= e_o), f"{what}: oracle closer to the long-double value at {int((e_k > e_o).sum())} px"
+    return len(bad)
 
 
 def test_fullband_config_c3(orc):
-    """BASELINE C3: 100x100x189 without DWT, LRX 15 (reference) and 15/5 guard; rows 0..6
-    and 47..52 compared with the oracle (kappa-aware: cond ~1e6-1e7 at 189 bands)."""
+    """BASELINE C3: 100x100x189 without DWT, every pixel of LRX 15 (reference), the 15/5
+    guard extension and DWRX 5/15, at the plain 1e-9 bar with the long-double third
+    opinion where the two fp64 solvers disagree (assert_plain_bar)."""
     cfg = CONFIGS["C3"]
     cube, _ = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], cfg["rate"],
                              device=DEV)
-    (l, _), (g, _) = [(host(s), c) for s, c in hs.detect_multi(
-        cube, [hs.DetectRequest("lrx", W1(15)), hs.DetectRequest("lrx", W1(15), guard=5)])]
+    (l, _), (g, _), (d, _) = [(host(s), c) for s, c in hs.detect_multi(
+        cube, [hs.DetectRequest("lrx", W1(15)), hs.DetectRequest("lrx", W1(15), guard=5),
+               hs.DetectRequest("dwrx", W2(5, 15))])]
     ch = host(cube)
-    for rows in ((0, 6), (47, 52)):
-        want = orc.port.local_rx(ch, 15, 1e-6, workers=8, rows=rows)
-        kap = _fb_kappa(ch.astype(np.float64), rows, 15, 1, 1e-6)
-        assert_kappa_close(l[rows[0]:rows[1]], want, kap, f"C3 lrx rows {rows}")
-        wg = orc.port.local_rx(ch, 15, 1e-6, guard=5, workers=8, rows=rows)
-        kg = _fb_kappa(ch.astype(np.float64), rows, 15, 5, 1e-6)
-        assert_kappa_close(g[rows[0]:rows[1]], wg, kg, f"C3 lrx guard rows {rows}")
+    assert_plain_bar(l, orc.port.local_rx(ch, 15, 1e-6, workers=16),
+                     lambda r, c: orc.port.hp_local_rx(ch, 15, r, c, workers=16)[0], "C3 lrx 15")
+    assert_plain_bar(g, orc.port.local_rx(ch, 15, 1e-6, guard=5, workers=16),
+                     lambda r, c: orc.port.hp_local_rx(ch, 15, r, c, guard=5, workers=16)[0],
+                     "C3 lrx 15 guard 5")
+    assert_plain_bar(d, orc.port.dwrx(ch, 5, 15, 1e-6, workers=16),
+                     lambda r, c: orc.port.hp_dwrx(ch, 5, 15, r, c, workers=16)[0], "C3 dwrx 5/15")
 
 
 def test_fullband_dwest_unsupported_and_errors(orc):
@@ -683,8 +655,10 @@ def test_maximum_window_and_limits(orc):
     w = lim.max_window
     cube = orc.port.random_cube(12, 17, 4, 4242)
     (l, _), (d, _) = run(cube, [hs.DetectRequest("lrx", W1(w)), hs.DetectRequest("dwrx", W2(w - 2, w))])
-    assert_kappa_close(l, orc.port.local_rx(cube, w), window_kappa(cube, w, 1, 1e-6), f"lrx {w}")
-    assert_kappa_close(d, orc.port.dwrx(cube, w - 2, w), window_kappa(cube, w, w - 2, 1e-6), f"dwrx {w}")
+    assert_plain_bar(l, orc.port.local_rx(cube, w), lambda r, c: orc.port.hp_local_rx(cube, w, r, c)[0],
+                     f"lrx {w}")
+    assert_plain_bar(d, orc.port.dwrx(cube, w - 2, w),
+                     lambda r, c: orc.port.hp_dwrx(cube, w - 2, w, r, c)[0], f"dwrx {w}")
     with pytest.raises(hs.HsadError) as e:
         run(cube, [hs.DetectRequest("lrx", W1(w + 2))])
     assert e.value.name == "Unsupported"

@@ -372,3 +372,24 @@ def test_oracle_matches_reference_golden_vectors(orc):
     assert max_rel_diff(orc.port.local_rx(cube, 7, 1e-6), g["lrx7_99"]) < 1e-10
     assert max_rel_diff(orc.port.dwrx(cube, 5, 9, 1e-6), g["dwrx59_99"]) < 1e-10
     assert max_rel_diff(orc.port.dwest(cube, 5, 9, 0.3)[0], g["dwest59_99"]) < 1e-10
+
+
+def test_long_double_third_opinion_pinned(orc):
+    """oracle/hp_oracle.cpp (long double) agrees with the fp64 restatement on
+    well-conditioned 4-band windows and reproduces the reference's hand case
+    (proj/tests/test_detect.cpp:76-91: LRX = 25 with ridge 1e-9)."""
+    cube = orc.port.random_cube(12, 13, 4, 2024)
+    rows, cols = np.divmod(np.arange(12 * 13), 13)
+    for window, guard in ((5, 1), (7, 3)):
+        want = orc.port.local_rx(cube, window, 1e-6, guard=guard)
+        got, piv = orc.port.hp_local_rx(cube, window, rows, cols, guard=guard)
+        assert orc.max_rel_diff(got.reshape(12, 13), want) < 1e-12
+        assert np.all(piv >= 1.0)
+    want = orc.port.dwrx(cube, 3, 7)
+    got, _ = orc.port.hp_dwrx(cube, 3, 7, rows, cols)
+    assert orc.max_rel_diff(got.reshape(12, 13), want) < 1e-12
+    hand = np.zeros((3, 3, 2))
+    hand[0, 0] = (2, 0); hand[0, 1] = (0, 2); hand[0, 2] = (-2, 0); hand[1, 0] = (0, -2)
+    hand[1, 1] = (3, 4)
+    got, _ = orc.port.hp_local_rx(hand, 3, np.array([1]), np.array([1]), ridge=1e-9)
+    assert abs(got[0] - 25.0) < 1e-6
