@@ -592,9 +592,10 @@ def run_b200(args, cfg, rank, world, local, dist):
             },
         },
         "clocks": clk,
-        # per step: 1 reduce + per window pair a fast detector pass and its zero-window
-        # counting pass (which exits at once on data without all-zero spectra)
-        "gpu_launches": (1 + 2 * len(SWEEP)) * args.steps,
+        # per step: 1 reduce + per window pair a fast detector pass, its zero-window
+        # counting pass (exits at once on data without all-zero spectra) and the
+        # accuracy-repair pass over the ill-conditioned-pixel bitmap
+        "gpu_launches": (1 + 3 * len(SWEEP)) * args.steps,
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:

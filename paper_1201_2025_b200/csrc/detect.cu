@@ -60,7 +60,10 @@ constexpr int kCodeOverflow = 0x80;
 #ifndef HSAD_PAIR_RADIUS
 #define HSAD_PAIR_RADIUS 2
 #endif
-constexpr int kPairRadius = HSAD_PAIR_RADIUS;  // flag: "inverse overflowed" variant of SingularAfterRidge
+constexpr int kPairRadius = HSAD_PAIR_RADIUS;
+// Pivot ratio of C + delta I above which an LRX / DWRX pixel is recomputed two-pass
+// (repair_kernel); HSAD_REPAIR_KAPPA overrides it (0 disables the repair).
+constexpr double kRepairKappa = 1e4;  // flag: "inverse overflowed" variant of SingularAfterRidge
 
 struct ReqDev {
     int algo;         // hsad_algorithm
@@ -95,6 +98,9 @@ struct DetectParams {
     double n_in, n_ann;  // standard-layout dual counts
     unsigned long long* status;
     int req_base;       // position of req[0] in the call's request list (failure ordering)
+    uint32_t* repair_bits;  // [nreq][repair_words]: LRX / DWRX pixels to recompute two-pass
+    int64_t repair_words;
+    double repair_kappa;    // pivot ratio of C + delta I above which a pixel is repaired
     int64_t diag_lin;   // >= 0: pixel whose ridge delta is written to diag_out ...
     int diag_req;       // ... by this request (call position) only
     double* diag_out;
@@ -250,7 +256,7 @@ __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n
 // Returns 0 or an error code.
 template <int L>
 __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L], double ridge,
-                                         double& score, double& delta) {
+                                         double& score, double& delta, double& ratio) {
     // a: upper triangle of C on entry; overwritten with U (C + delta I = U^T U)
     double tr = 0.0;
 #pragma unroll
@@ -283,6 +289,7 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
         z[j] = zj * rinv;
     }
     if (!ok || !(dmax > 0.0) || dmin <= dmax * 1e-14) return HSAD_E_SINGULAR_AFTER_RIDGE;
+    ratio = dmax * fast_rcp(dmin);
     double s = 0.0;
 #pragma unroll
     for (int j = 0; j < L; ++j) s = fma(z[j], z[j], s);
@@ -567,6 +574,15 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
     for (int i = 0; i < L; ++i) w[i] = B[i][i];
 }
 
+// Ill-conditioned windows (pivot ratio of C + delta I above P.repair_kappa): the shifted
+// one-pass covariance S2/N - mu mu^T carries ~|y|^2/|C| times the rounding of the
+// reference's two-pass form, amplified by the conditioning, so those pixels are
+// marked here and recomputed two-pass by repair_kernel (rare on real scenes).
+__device__ __forceinline__ void flag_repair(const DetectParams& P, int q, int64_t o, double ratio) {
+    if (P.repair_bits && ratio > P.repair_kappa)
+        atomicOr(P.repair_bits + q * P.repair_words + (o >> 5), 1u << (o & 31));
+}
+
 __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s) {
     if (R.score_bytes == 8) static_cast<double*>(R.scores)[o] = s;
     else static_cast<float*>(R.scores)[o] = static_cast<float>(s);
@@ -595,8 +611,9 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const Re
     }
     double score = 0.0;
     if (dmax > 0.0) {
-        double delta = 0.0;
-        const int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
+        double delta = 0.0, ratio = 0.0;
+        const int code = chol_quad<L>(cm, dv, R.ridge, score, delta, ratio);
+        if (!code) flag_repair(P, q, o, ratio);
         if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
             report(P, q, r, col, code);
@@ -647,8 +664,9 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const R
         for (int i = 0; i < L; ++i)
 #pragma unroll
             for (int j = i; j < L; ++j) a[i][j] = D.c_out[i][j];
-        double delta = 0.0;
-        const int code = chol_quad<L>(a, D.md, R.ridge, score, delta);
+        double delta = 0.0, ratio = 0.0;
+        const int code = chol_quad<L>(a, D.md, R.ridge, score, delta, ratio);
+        if (!code) flag_repair(P, q, o, ratio);
         if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
             report(P, q, r, col, code);
@@ -793,6 +811,112 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                 if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, q, R, D, r, col, o, lin);
                 else dwest_solve<L>(R, D, o);
             }
+        }
+    }
+}
+
+// ---- accuracy repair of ill-conditioned LRX / DWRX pixels ----------------------------
+// Recomputes the pixels flag_repair marked with the reference's own arithmetic: the
+// window gathered in its row-major scan order (detect.cpp:83-117, reflection on global
+// coordinates), mean, two-pass centred covariance / N (stats.cpp:7-29), ridge
+// delta = ridge tr(C) / L, then the same Cholesky quadratic form and singular rule as
+// chol_quad. One thread per 32-pixel word of the flag bitmap (flags are sparse).
+template <int L>
+__device__ __forceinline__ void load_px(const DetectParams& P, int64_t r, int64_t c, double (&x)[L]) {
+    const int64_t rr = mirror_index(r, P.lines) - P.buf_row0;
+    const int64_t cc = mirror_index(c, P.samples);
+    const int64_t i = (rr * P.samples + cc) * L;
+    if (P.elem_bytes == 8) {
+#pragma unroll
+        for (int b = 0; b < L; ++b) x[b] = static_cast<const double*>(P.cube)[i + b];
+    } else {
+#pragma unroll
+        for (int b = 0; b < L; ++b) x[b] = static_cast<double>(static_cast<const float*>(P.cube)[i + b]);
+    }
+}
+
+// window samples: |dr|, |dc| <= outer, minus |dr|, |dc| <= hole (hole < 0: none)
+template <int L, typename Fn>
+__device__ __forceinline__ void for_window(const DetectParams& P, int64_t r, int64_t c, int outer, int hole,
+                                           Fn&& fn) {
+    for (int dr = -outer; dr <= outer; ++dr)
+        for (int dc = -outer; dc <= outer; ++dc) {
+            if (abs(dr) <= hole && abs(dc) <= hole) continue;
+            double x[L];
+            load_px<L>(P, r + dr, c + dc, x);
+            fn(x);
+        }
+}
+
+template <int L>
+__device__ __forceinline__ void window_mean_cov(const DetectParams& P, int64_t r, int64_t c, int outer,
+                                                int hole, double n, double (&mu)[L], double (&cv)[L][L]) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) mu[i] = 0.0;
+    for_window<L>(P, r, c, outer, hole, [&](const double (&x)[L]) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) mu[i] += x[i];
+    });
+#pragma unroll
+    for (int i = 0; i < L; ++i) mu[i] /= n;
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) cv[i][j] = 0.0;
+    for_window<L>(P, r, c, outer, hole, [&](const double (&x)[L]) {
+        double d[L];
+#pragma unroll
+        for (int i = 0; i < L; ++i) d[i] = x[i] - mu[i];
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+#pragma unroll
+            for (int j = i; j < L; ++j) cv[i][j] = fma(d[i], d[j], cv[i][j]);
+    });
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) cv[i][j] /= n;
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) repair_kernel(const DetectParams P) {
+    const int64_t npix = (P.row_end - P.row_begin) * P.samples;
+    const int64_t total = P.nreq * P.repair_words;
+    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t bits = P.repair_bits[w];
+        const int q = static_cast<int>(w / P.repair_words);
+        const ReqDev& R = P.req[q];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t o = (w % P.repair_words) * 32 + b;
+            if (o >= npix) break;
+            const int64_t r = P.row_begin + o / P.samples, col = o % P.samples;
+            double mu[L], cv[L][L], d[L];
+            if (R.algo == HSAD_LRX) {
+                const int hole = R.box_b < 0 ? 0 : P.radius[R.box_b];
+                window_mean_cov<L>(P, r, col, P.radius[R.box_a], hole, R.n_a, mu, cv);
+                double x[L];
+                load_px<L>(P, r, col, x);
+#pragma unroll
+                for (int i = 0; i < L; ++i) d[i] = x[i] - mu[i];
+            } else {
+                double mu_in[L], cin[L][L];
+                window_mean_cov<L>(P, r, col, P.radius[R.box_b], -1, R.n_a, mu_in, cin);
+                window_mean_cov<L>(P, r, col, P.radius[R.box_a], P.radius[R.box_b], R.n_b, mu, cv);
+#pragma unroll
+                for (int i = 0; i < L; ++i) d[i] = mu_in[i] - mu[i];
+            }
+            double score = 0.0, delta = 0.0, ratio = 0.0, dmax = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) dmax = fmax(dmax, fabs(d[i]));
+            const int code = dmax > 0.0 ? chol_quad<L>(cv, d, R.ridge, score, delta, ratio) : 0;
+            if (code) {
+                atomicMin(P.status, pack_failure(P.req_base + q, r * P.samples + col, code));
+                score = 0.0;
+            }
+            store_score(R, o, R.algo == HSAD_LRX ? fmax(score, 0.0) : fabs(score));
         }
     }
 }
@@ -1213,6 +1337,24 @@ cudaError_t launch_detect(int bands, const DetectParams& P0, dim3 grid, int nt, 
     return e;
 }
 
+cudaError_t launch_repair(int bands, const DetectParams& P, cudaStream_t s) {
+    const int64_t total = P.nreq * P.repair_words;
+    const int64_t want = (total + 127) / 128;
+    const int grid = static_cast<int>(want < 148 * 8 ? (want < 1 ? 1 : want) : 148 * 8);
+    switch (bands) {
+        case 1: repair_kernel<1><<<grid, 128, 0, s>>>(P); break;
+        case 2: repair_kernel<2><<<grid, 128, 0, s>>>(P); break;
+        case 3: repair_kernel<3><<<grid, 128, 0, s>>>(P); break;
+        case 4: repair_kernel<4><<<grid, 128, 0, s>>>(P); break;
+        case 5: repair_kernel<5><<<grid, 128, 0, s>>>(P); break;
+        case 6: repair_kernel<6><<<grid, 128, 0, s>>>(P); break;
+        case 7: repair_kernel<7><<<grid, 128, 0, s>>>(P); break;
+        case 8: repair_kernel<8><<<grid, 128, 0, s>>>(P); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 const char* algo_name(int a) {
     return a == HSAD_LRX ? "local_rx" : a == HSAD_DWRX ? "dwrx" : a == HSAD_DWEST ? "dwest" : "?";
 }
@@ -1437,6 +1579,9 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                    smem_cap &&
                !getenv("HSAD_NO_STAGE");
     P.req_base = req_base;
+    P.repair_bits = nullptr;
+    P.repair_words = 0;
+    P.repair_kappa = getenv("HSAD_REPAIR_KAPPA") ? atof(getenv("HSAD_REPAIR_KAPPA")) : kRepairKappa;
     P.diag_lin = -1;
     P.diag_req = -1;
     P.diag_out = nullptr;
@@ -1493,8 +1638,24 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         hsad_status fst = launch_fb(row_begin, row_end, -1, -1, nullptr, nullptr);
         if (fst != HSAD_OK) return fst;
     } else {
+        // accuracy-repair bitmap for the LRX / DWRX requests (one bit per output pixel)
+        bool any_rx = false;
+        for (int q = 0; q < n_requests; ++q) any_rx = any_rx || requests[q].algorithm != HSAD_DWEST;
+        ScratchGuard repair_guard(s);
+        if (any_rx && P.repair_kappa > 0.0) {
+            P.repair_words = ((row_end - row_begin) * samples + 31) / 32;
+            const size_t bytes = static_cast<size_t>(P.nreq) * P.repair_words * sizeof(uint32_t);
+            HSAD_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&P.repair_bits), bytes, s));
+            repair_guard.p = P.repair_bits;
+            HSAD_CUDA_TRY(cudaMemsetAsync(P.repair_bits, 0, bytes, s));
+        }
         e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
         if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
+        if (P.repair_bits) {
+            e = launch_repair(bands, P, s);
+            if (e != cudaSuccess) return cuda_fail(e, "hsad detect repair launch");
+        }
+        P.repair_bits = nullptr;  // freed with the guard; the diagnostic re-run does not repair
     }
     if (!sync) return HSAD_OK;
 
