@@ -62,8 +62,9 @@ constexpr int kCodeOverflow = 0x80;
 #endif
 constexpr int kPairRadius = HSAD_PAIR_RADIUS;
 // Pivot ratio of C + delta I above which an LRX / DWRX pixel is recomputed two-pass
-// (repair_kernel); HSAD_REPAIR_KAPPA overrides it (0 disables the repair).
-constexpr double kRepairKappa = 1e4;  // flag: "inverse overflowed" variant of SingularAfterRidge
+// (repair_pixel, in the counting pass).
+constexpr double kRepairKappa = 1e4;
+constexpr int kIllConditioned = 0x100;  // chol_quad: solved, but flag the pixel for the repair
 
 struct ReqDev {
     int algo;         // hsad_algorithm
@@ -98,9 +99,6 @@ struct DetectParams {
     double n_in, n_ann;  // standard-layout dual counts
     unsigned long long* status;
     int req_base;       // position of req[0] in the call's request list (failure ordering)
-    uint32_t* repair_bits;  // [nreq][repair_words]: LRX / DWRX pixels to recompute two-pass
-    int64_t repair_words;
-    double repair_kappa;    // pivot ratio of C + delta I above which a pixel is repaired
     int64_t diag_lin;   // >= 0: pixel whose ridge delta is written to diag_out ...
     int diag_req;       // ... by this request (call position) only
     double* diag_out;
@@ -241,7 +239,7 @@ __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n
                                          double (&c)[L][L], bool zero) {
     const double inv = fast_rcp(n);
 #pragma unroll
-    for (int i = 0; i < L; ++i) mu[i] = s[i] * inv;
+    for (int i = 0; i < L; ++i) mu[i] = __dmul_rn(s[i], inv);  // never fused into the uses
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
@@ -256,12 +254,12 @@ __device__ __forceinline__ void mean_cov(const double (&s)[Dim<L>::NC], double n
 // Returns 0 or an error code.
 template <int L>
 __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L], double ridge,
-                                         double& score, double& delta, double& ratio) {
+                                         double& score, double& delta) {
     // a: upper triangle of C on entry; overwritten with U (C + delta I = U^T U)
     double tr = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i) tr += a[i][i];
-    delta = (L & (L - 1)) == 0 ? ridge * tr * (1.0 / L) : ridge * tr / static_cast<double>(L);
+    delta = (L & (L - 1)) == 0 ? __dmul_rn(__dmul_rn(ridge, tr), 1.0 / L) : __ddiv_rn(__dmul_rn(ridge, tr), L);
 #pragma unroll
     for (int i = 0; i < L; ++i) a[i][i] += delta;
     double dmax = 0.0, dmin = DBL_MAX;
@@ -289,15 +287,25 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
         z[j] = zj * rinv;
     }
     if (!ok || !(dmax > 0.0) || dmin <= dmax * 1e-14) return HSAD_E_SINGULAR_AFTER_RIDGE;
-    ratio = dmax * fast_rcp(dmin);
     double s = 0.0;
 #pragma unroll
     for (int j = 0; j < L; ++j) s = fma(z[j], z[j], s);
     if (!isfinite(s)) return HSAD_E_SINGULAR_AFTER_RIDGE | kCodeOverflow;
     score = s;
+#ifdef HSAD_NO_REPAIR
     return 0;
+#else
+    return dmax > kRepairKappa * dmin ? kIllConditioned : 0;
+#endif
 }
 
+
+// Explicit fused multiply-add for float and double. Every product that feeds a sum on
+// the score path is either fused here or formed with a __dmul_rn intrinsic (which
+// the compiler never contracts), so all kernel instantiations round identically:
+// the staged and the global-load kernels must produce bit-identical maps.
+__device__ __forceinline__ float mad(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double mad(double a, double b, double c) { return __fma_rn(a, b, c); }
 
 // Symmetric L x L matrices are kept as their upper triangle only (a[i][j], i <= j);
 // sym(a, i, j) addresses element (i, j) for any order with compile-time indices,
@@ -313,8 +321,8 @@ template <int L, typename T>
 __device__ __forceinline__ void rotate_tc(T (&a)[L][L], T (&v)[L][L], int p, int q, T t, T c) {
     const T apq = a[p][q];
     const T s = t * c;
-    a[p][p] -= t * apq;
-    a[q][q] += t * apq;
+    a[p][p] = mad(-t, apq, a[p][p]);
+    a[q][q] = mad(t, apq, a[q][q]);
     a[p][q] = T(0);
 #pragma unroll
     for (int k = 0; k < L; ++k) {
@@ -322,14 +330,14 @@ __device__ __forceinline__ void rotate_tc(T (&a)[L][L], T (&v)[L][L], int p, int
         T& akp = sym<L, T>(a, k, p);
         T& akq = sym<L, T>(a, k, q);
         const T x = akp, y = akq;
-        akp = c * x - s * y;
-        akq = s * x + c * y;
+        akp = mad(c, x, -(s * y));
+        akq = mad(s, x, c * y);
     }
 #pragma unroll
     for (int k = 0; k < L; ++k) {
         const T vkp = v[k][p], vkq = v[k][q];
-        v[k][p] = c * vkp - s * vkq;
-        v[k][q] = s * vkp + c * vkq;
+        v[k][p] = mad(c, vkp, -(s * vkq));
+        v[k][q] = mad(s, vkp, c * vkq);
     }
 }
 
@@ -348,7 +356,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 __device__ __forceinline__ float jacobi_t32(float app, float aqq, float apq) {
     const float h = aqq - app;
     const float r2 = fmaf(4.0f * apq, apq, h * h);
-    const float den = fabsf(h) + r2 * rsqrtf(r2);
+    const float den = mad(r2, rsqrtf(r2), fabsf(h));
     float t = 2.0f * apq * rcp_approx(den);
     t = h < 0.0f ? -t : t;
     return den > 0.0f ? t : 0.0f;
@@ -358,7 +366,7 @@ __device__ __forceinline__ float jacobi_t32(float app, float aqq, float apq) {
 __device__ __forceinline__ double jacobi_t64(double app, double aqq, double apq) {
     const double h = aqq - app;
     const double r2 = fma(4.0 * apq, apq, h * h);
-    const double den = fabs(h) + r2 * fast_rsqrt(r2);
+    const double den = mad(r2, fast_rsqrt(r2), fabs(h));
     double t = 2.0 * apq * fast_rcp(den);
     t = h < 0.0 ? -t : t;
     return den > 0.0 ? t : 0.0;
@@ -412,8 +420,8 @@ __device__ __forceinline__ void sweep32_4(float (&a)[4][4], float2 (&vv)[4][2]) 
         const float c = rsqrtf(fmaf(t, t, 1.0f));
         const float s = t * c;
         const float apq = a[p][q];
-        a[p][p] -= t * apq;
-        a[q][q] += t * apq;
+        a[p][p] = mad(-t, apq, a[p][p]);
+        a[q][q] = mad(t, apq, a[q][q]);
         a[p][q] = 0.0f;
         const float2 c2 = make_float2(c, c), s2 = make_float2(s, s), ns2 = make_float2(-s, -s);
 #pragma unroll
@@ -422,8 +430,8 @@ __device__ __forceinline__ void sweep32_4(float (&a)[4][4], float2 (&vv)[4][2]) 
             float& akp = sym<4, float>(a, k, p);
             float& akq = sym<4, float>(a, k, q);
             const float x = akp, y = akq;
-            akp = c * x - s * y;
-            akq = s * x + c * y;
+            akp = mad(c, x, -(s * y));
+            akq = mad(s, x, c * y);
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -574,24 +582,111 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
     for (int i = 0; i < L; ++i) w[i] = B[i][i];
 }
 
-// Ill-conditioned windows (pivot ratio of C + delta I above P.repair_kappa): the shifted
-// one-pass covariance S2/N - mu mu^T carries ~|y|^2/|C| times the rounding of the
-// reference's two-pass form, amplified by the conditioning, so those pixels are
-// marked here and recomputed two-pass by repair_kernel (rare on real scenes).
-__device__ __forceinline__ void flag_repair(const DetectParams& P, int q, int64_t o, double ratio) {
-    if (P.repair_bits && ratio > P.repair_kappa)
-        atomicOr(P.repair_bits + q * P.repair_words + (o >> 5), 1u << (o & 31));
-}
-
 __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s) {
     if (R.score_bytes == 8) static_cast<double*>(R.scores)[o] = s;
     else static_cast<float*>(R.scores)[o] = static_cast<float>(s);
 }
 
+// ---- accuracy repair of ill-conditioned LRX / DWRX pixels ----------------------------
+// The shifted one-pass covariance S2/N - mu mu^T carries ~|y|^2/|C| times the rounding
+// of the reference's two-pass form, and an ill-conditioned C + delta I amplifies it. A
+// pixel whose Cholesky pivot ratio exceeds kRepairKappa is therefore recomputed with
+// the reference's own arithmetic: the window gathered in its row-major scan order
+// (detect.cpp:83-117, reflection on global coordinates), mean, two-pass centred
+// covariance / N (stats.cpp:7-29), then the same ridge, Cholesky quadratic form and
+// singular rule. The fast pass only marks the CTA (like a zero spectrum); the counting
+// pass, which recomputes marked CTAs, repairs such pixels in place. Rare on real
+// scenes (none on the C5 sweep), common only in sample-starved windows (3x3 boxes at
+// mirrored corners).
+template <int L>
+__device__ __forceinline__ void load_px(const DetectParams& P, int64_t r, int64_t c, double (&x)[L]) {
+    const int64_t rr = mirror_index(r, P.lines) - P.buf_row0;
+    const int64_t cc = mirror_index(c, P.samples);
+    const int64_t i = (rr * P.samples + cc) * L;
+    if (P.elem_bytes == 8) {
+#pragma unroll
+        for (int b = 0; b < L; ++b) x[b] = static_cast<const double*>(P.cube)[i + b];
+    } else {
+#pragma unroll
+        for (int b = 0; b < L; ++b) x[b] = static_cast<double>(static_cast<const float*>(P.cube)[i + b]);
+    }
+}
+
+// window samples: |dr|, |dc| <= outer, minus |dr|, |dc| <= hole (hole < 0: none)
+template <int L, typename Fn>
+__device__ __forceinline__ void for_window(const DetectParams& P, int64_t r, int64_t c, int outer, int hole,
+                                           Fn&& fn) {
+    for (int dr = -outer; dr <= outer; ++dr)
+        for (int dc = -outer; dc <= outer; ++dc) {
+            if (abs(dr) <= hole && abs(dc) <= hole) continue;
+            double x[L];
+            load_px<L>(P, r + dr, c + dc, x);
+            fn(x);
+        }
+}
+
+template <int L>
+__device__ __forceinline__ void window_mean_cov(const DetectParams& P, int64_t r, int64_t c, int outer,
+                                                int hole, double n, double (&mu)[L], double (&cv)[L][L]) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) mu[i] = 0.0;
+    for_window<L>(P, r, c, outer, hole, [&](const double (&x)[L]) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) mu[i] += x[i];
+    });
+#pragma unroll
+    for (int i = 0; i < L; ++i) mu[i] /= n;
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) cv[i][j] = 0.0;
+    for_window<L>(P, r, c, outer, hole, [&](const double (&x)[L]) {
+        double d[L];
+#pragma unroll
+        for (int i = 0; i < L; ++i) d[i] = x[i] - mu[i];
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+#pragma unroll
+            for (int j = i; j < L; ++j) cv[i][j] = fma(d[i], d[j], cv[i][j]);
+    });
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) cv[i][j] /= n;
+}
+
+// Two-pass LRX / DWRX score of one pixel (returns 0 or an error code).
+template <int L>
+__device__ __noinline__ int repair_pixel(const DetectParams& P, const ReqDev& R, int64_t r, int64_t col,
+                                         double& score) {
+    double mu[L], cv[L][L], d[L];
+    if (R.algo == HSAD_LRX) {
+        const int hole = R.box_b < 0 ? 0 : P.radius[R.box_b];
+        window_mean_cov<L>(P, r, col, P.radius[R.box_a], hole, R.n_a, mu, cv);
+        double x[L];
+        load_px<L>(P, r, col, x);
+#pragma unroll
+        for (int i = 0; i < L; ++i) d[i] = x[i] - mu[i];
+    } else {
+        double mu_in[L], cin[L][L];
+        window_mean_cov<L>(P, r, col, P.radius[R.box_b], -1, R.n_a, mu_in, cin);
+        window_mean_cov<L>(P, r, col, P.radius[R.box_a], P.radius[R.box_b], R.n_b, mu, cv);
+#pragma unroll
+        for (int i = 0; i < L; ++i) d[i] = mu_in[i] - mu[i];
+    }
+    double dmax = 0.0, delta = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) dmax = fmax(dmax, fabs(d[i]));
+    score = 0.0;
+    if (!(dmax > 0.0)) return 0;
+    const int code = chol_quad<L>(cv, d, R.ridge, score, delta);
+    return code == kIllConditioned ? 0 : code;
+}
+
 // ---- per-detector solves on window statistics ---------------------------------
 
 // LRX (detect.cpp:168-188) on background sums bg, count n: score = max(d^T (C+dI)^-1 d, 0)
-template <int L>
+template <int L, bool ZC>
 __device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const ReqDev& R,
                                           const double (&bg)[Dim<L>::NC], double n_bg, bool bg_zero,
                                           int nzc, const double (&yc)[L], int64_t r, int64_t col,
@@ -611,9 +706,12 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const Re
     }
     double score = 0.0;
     if (dmax > 0.0) {
-        double delta = 0.0, ratio = 0.0;
-        const int code = chol_quad<L>(cm, dv, R.ridge, score, delta, ratio);
-        if (!code) flag_repair(P, q, o, ratio);
+        double delta = 0.0;
+        int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
+        if (code == kIllConditioned) {
+            if constexpr (ZC) code = repair_pixel<L>(P, R, r, col, score);
+            else s_zero_seen = 1, code = 0;  // the counting pass recomputes this CTA
+        }
         if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
             report(P, q, r, col, code);
@@ -653,7 +751,7 @@ __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
 }
 
 // DWRX (detect.cpp:204-223): |m^T (C_ann + dI)^-1 m|
-template <int L>
+template <int L, bool ZC>
 __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const ReqDev& R,
                                            const DualStats<L>& D, int64_t r, int64_t col, int64_t o,
                                            int64_t lin) {
@@ -664,9 +762,12 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const R
         for (int i = 0; i < L; ++i)
 #pragma unroll
             for (int j = i; j < L; ++j) a[i][j] = D.c_out[i][j];
-        double delta = 0.0, ratio = 0.0;
-        const int code = chol_quad<L>(a, D.md, R.ridge, score, delta, ratio);
-        if (!code) flag_repair(P, q, o, ratio);
+        double delta = 0.0;
+        int code = chol_quad<L>(a, D.md, R.ridge, score, delta);
+        if (code == kIllConditioned) {
+            if constexpr (ZC) code = repair_pixel<L>(P, R, r, col, score);
+            else s_zero_seen = 1, code = 0;  // the counting pass recomputes this CTA
+        }
         if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
             report(P, q, r, col, code);
@@ -758,7 +859,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
 #pragma unroll
             for (int c = 0; c < NC; ++c) bg[c] = S[0][c];
             add_moments<L>(bg, yc, -1.0);
-            lrx_solve<L>(P, q, R, bg, R.n_a, ZC && cnt[0] - nzc == 0, nzc, yc, r, col, o, lin);
+            lrx_solve<L, ZC>(P, q, R, bg, R.n_a, ZC && cnt[0] - nzc == 0, nzc, yc, r, col, o, lin);
         }
 #ifdef HSAD_PHASE_TIMERS
         long long q0 = clock64();  // phases 5/6 sampled on thread 0 of each CTA (x128)
@@ -768,7 +869,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                 DualStats<L> D;
                 dual_stats<L>(S[1], S[0], P.n_in, P.n_ann, ZC && cnt[1] == 0, ZC && cnt[0] - cnt[1] == 0, D);
                 for (int q = 0; q < P.nreq; ++q)  // DWRX first: C_ann dies before the eigensolve
-                    if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L>(P, q, s_req[q], D, r, col, o, lin);
+                    if (s_req[q].algo == HSAD_DWRX) dwrx_solve<L, ZC>(P, q, s_req[q], D, r, col, o, lin);
 #ifdef HSAD_PHASE_TIMERS
                 long long q1 = clock64();
                 if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[5], 128ull * (q1 - q0));
@@ -799,7 +900,7 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                     for (int c = 0; c < NC; ++c) bg[c] -= g[c];
                     nz_bg -= select_cnt<NBOX>(cnt, R.box_b);
                 }
-                lrx_solve<L>(P, q, R, bg, R.n_a, ZC && nz_bg == 0, nzc, yc, r, col, o, lin);
+                lrx_solve<L, ZC>(P, q, R, bg, R.n_a, ZC && nz_bg == 0, nzc, yc, r, col, o, lin);
             } else {
                 double s_in[NC], s_box[NC];
                 select_box<L, NBOX>(S, R.box_b, s_in);
@@ -808,115 +909,9 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
                 const int nz_box = select_cnt<NBOX>(cnt, R.box_a);
                 DualStats<L> D;
                 dual_stats<L>(s_in, s_box, R.n_a, R.n_b, ZC && nz_in == 0, ZC && nz_box - nz_in == 0, D);
-                if (R.algo == HSAD_DWRX) dwrx_solve<L>(P, q, R, D, r, col, o, lin);
+                if (R.algo == HSAD_DWRX) dwrx_solve<L, ZC>(P, q, R, D, r, col, o, lin);
                 else dwest_solve<L>(R, D, o);
             }
-        }
-    }
-}
-
-// ---- accuracy repair of ill-conditioned LRX / DWRX pixels ----------------------------
-// Recomputes the pixels flag_repair marked with the reference's own arithmetic: the
-// window gathered in its row-major scan order (detect.cpp:83-117, reflection on global
-// coordinates), mean, two-pass centred covariance / N (stats.cpp:7-29), ridge
-// delta = ridge tr(C) / L, then the same Cholesky quadratic form and singular rule as
-// chol_quad. One thread per 32-pixel word of the flag bitmap (flags are sparse).
-template <int L>
-__device__ __forceinline__ void load_px(const DetectParams& P, int64_t r, int64_t c, double (&x)[L]) {
-    const int64_t rr = mirror_index(r, P.lines) - P.buf_row0;
-    const int64_t cc = mirror_index(c, P.samples);
-    const int64_t i = (rr * P.samples + cc) * L;
-    if (P.elem_bytes == 8) {
-#pragma unroll
-        for (int b = 0; b < L; ++b) x[b] = static_cast<const double*>(P.cube)[i + b];
-    } else {
-#pragma unroll
-        for (int b = 0; b < L; ++b) x[b] = static_cast<double>(static_cast<const float*>(P.cube)[i + b]);
-    }
-}
-
-// window samples: |dr|, |dc| <= outer, minus |dr|, |dc| <= hole (hole < 0: none)
-template <int L, typename Fn>
-__device__ __forceinline__ void for_window(const DetectParams& P, int64_t r, int64_t c, int outer, int hole,
-                                           Fn&& fn) {
-    for (int dr = -outer; dr <= outer; ++dr)
-        for (int dc = -outer; dc <= outer; ++dc) {
-            if (abs(dr) <= hole && abs(dc) <= hole) continue;
-            double x[L];
-            load_px<L>(P, r + dr, c + dc, x);
-            fn(x);
-        }
-}
-
-template <int L>
-__device__ __forceinline__ void window_mean_cov(const DetectParams& P, int64_t r, int64_t c, int outer,
-                                                int hole, double n, double (&mu)[L], double (&cv)[L][L]) {
-#pragma unroll
-    for (int i = 0; i < L; ++i) mu[i] = 0.0;
-    for_window<L>(P, r, c, outer, hole, [&](const double (&x)[L]) {
-#pragma unroll
-        for (int i = 0; i < L; ++i) mu[i] += x[i];
-    });
-#pragma unroll
-    for (int i = 0; i < L; ++i) mu[i] /= n;
-#pragma unroll
-    for (int i = 0; i < L; ++i)
-#pragma unroll
-        for (int j = i; j < L; ++j) cv[i][j] = 0.0;
-    for_window<L>(P, r, c, outer, hole, [&](const double (&x)[L]) {
-        double d[L];
-#pragma unroll
-        for (int i = 0; i < L; ++i) d[i] = x[i] - mu[i];
-#pragma unroll
-        for (int i = 0; i < L; ++i)
-#pragma unroll
-            for (int j = i; j < L; ++j) cv[i][j] = fma(d[i], d[j], cv[i][j]);
-    });
-#pragma unroll
-    for (int i = 0; i < L; ++i)
-#pragma unroll
-        for (int j = i; j < L; ++j) cv[i][j] /= n;
-}
-
-template <int L>
-__global__ void __launch_bounds__(128) repair_kernel(const DetectParams P) {
-    const int64_t npix = (P.row_end - P.row_begin) * P.samples;
-    const int64_t total = P.nreq * P.repair_words;
-    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
-         w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        uint32_t bits = P.repair_bits[w];
-        const int q = static_cast<int>(w / P.repair_words);
-        const ReqDev& R = P.req[q];
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int64_t o = (w % P.repair_words) * 32 + b;
-            if (o >= npix) break;
-            const int64_t r = P.row_begin + o / P.samples, col = o % P.samples;
-            double mu[L], cv[L][L], d[L];
-            if (R.algo == HSAD_LRX) {
-                const int hole = R.box_b < 0 ? 0 : P.radius[R.box_b];
-                window_mean_cov<L>(P, r, col, P.radius[R.box_a], hole, R.n_a, mu, cv);
-                double x[L];
-                load_px<L>(P, r, col, x);
-#pragma unroll
-                for (int i = 0; i < L; ++i) d[i] = x[i] - mu[i];
-            } else {
-                double mu_in[L], cin[L][L];
-                window_mean_cov<L>(P, r, col, P.radius[R.box_b], -1, R.n_a, mu_in, cin);
-                window_mean_cov<L>(P, r, col, P.radius[R.box_a], P.radius[R.box_b], R.n_b, mu, cv);
-#pragma unroll
-                for (int i = 0; i < L; ++i) d[i] = mu_in[i] - mu[i];
-            }
-            double score = 0.0, delta = 0.0, ratio = 0.0, dmax = 0.0;
-#pragma unroll
-            for (int i = 0; i < L; ++i) dmax = fmax(dmax, fabs(d[i]));
-            const int code = dmax > 0.0 ? chol_quad<L>(cv, d, R.ridge, score, delta, ratio) : 0;
-            if (code) {
-                atomicMin(P.status, pack_failure(P.req_base + q, r * P.samples + col, code));
-                score = 0.0;
-            }
-            store_score(R, o, R.algo == HSAD_LRX ? fmax(score, 0.0) : fabs(score));
         }
     }
 }
@@ -1337,24 +1332,6 @@ cudaError_t launch_detect(int bands, const DetectParams& P0, dim3 grid, int nt, 
     return e;
 }
 
-cudaError_t launch_repair(int bands, const DetectParams& P, cudaStream_t s) {
-    const int64_t total = P.nreq * P.repair_words;
-    const int64_t want = (total + 127) / 128;
-    const int grid = static_cast<int>(want < 148 * 8 ? (want < 1 ? 1 : want) : 148 * 8);
-    switch (bands) {
-        case 1: repair_kernel<1><<<grid, 128, 0, s>>>(P); break;
-        case 2: repair_kernel<2><<<grid, 128, 0, s>>>(P); break;
-        case 3: repair_kernel<3><<<grid, 128, 0, s>>>(P); break;
-        case 4: repair_kernel<4><<<grid, 128, 0, s>>>(P); break;
-        case 5: repair_kernel<5><<<grid, 128, 0, s>>>(P); break;
-        case 6: repair_kernel<6><<<grid, 128, 0, s>>>(P); break;
-        case 7: repair_kernel<7><<<grid, 128, 0, s>>>(P); break;
-        case 8: repair_kernel<8><<<grid, 128, 0, s>>>(P); break;
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-}
-
 const char* algo_name(int a) {
     return a == HSAD_LRX ? "local_rx" : a == HSAD_DWRX ? "dwrx" : a == HSAD_DWEST ? "dwest" : "?";
 }
@@ -1579,9 +1556,6 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                    smem_cap &&
                !getenv("HSAD_NO_STAGE");
     P.req_base = req_base;
-    P.repair_bits = nullptr;
-    P.repair_words = 0;
-    P.repair_kappa = getenv("HSAD_REPAIR_KAPPA") ? atof(getenv("HSAD_REPAIR_KAPPA")) : kRepairKappa;
     P.diag_lin = -1;
     P.diag_req = -1;
     P.diag_out = nullptr;
@@ -1638,24 +1612,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         hsad_status fst = launch_fb(row_begin, row_end, -1, -1, nullptr, nullptr);
         if (fst != HSAD_OK) return fst;
     } else {
-        // accuracy-repair bitmap for the LRX / DWRX requests (one bit per output pixel)
-        bool any_rx = false;
-        for (int q = 0; q < n_requests; ++q) any_rx = any_rx || requests[q].algorithm != HSAD_DWEST;
-        ScratchGuard repair_guard(s);
-        if (any_rx && P.repair_kappa > 0.0) {
-            P.repair_words = ((row_end - row_begin) * samples + 31) / 32;
-            const size_t bytes = static_cast<size_t>(P.nreq) * P.repair_words * sizeof(uint32_t);
-            HSAD_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&P.repair_bits), bytes, s));
-            repair_guard.p = P.repair_bits;
-            HSAD_CUDA_TRY(cudaMemsetAsync(P.repair_bits, 0, bytes, s));
-        }
         e = launch_detect(bands, P, plan.grid, plan.nt, plan.kcols, s);
         if (e != cudaSuccess) return cuda_fail(e, "hsad detect kernel launch");
-        if (P.repair_bits) {
-            e = launch_repair(bands, P, s);
-            if (e != cudaSuccess) return cuda_fail(e, "hsad detect repair launch");
-        }
-        P.repair_bits = nullptr;  // freed with the guard; the diagnostic re-run does not repair
     }
     if (!sync) return HSAD_OK;
 

@@ -2,7 +2,7 @@
 
     python scripts/probe_repair.py
 Runs the C5 sweep detectors with the repair on (default threshold) and off
-(HSAD_REPAIR_KAPPA=0 is read per call) and counts pixels whose scores differ."""
+(HSAD_NO_REPAIR=1 is read per call) and counts pixels whose scores differ."""
 import os
 import sys
 from pathlib import Path
@@ -23,8 +23,8 @@ for inner, outer in [(3, 7), (5, 11), (5, 15), (7, 21)]:
     reqs = [hs.DetectRequest("lrx", W1(outer)), hs.DetectRequest("dwrx", W2(inner, outer)),
             hs.DetectRequest("dwest", W2(inner, outer), eigcount=True)]
     res = {}
-    for kappa in ("1e4", "0"):
-        os.environ["HSAD_REPAIR_KAPPA"] = kappa
+    for kappa in ("on", "off"):
+        os.environ.pop("HSAD_NO_REPAIR", None) if kappa == "on" else os.environ.__setitem__("HSAD_NO_REPAIR", "1")
         st = torch.full((1,), -1, dtype=torch.int64, device="cuda")
         outs = hs.detect_multi(red, reqs, status=st)
         for _ in range(2):
@@ -35,6 +35,6 @@ for inner, outer in [(3, 7), (5, 11), (5, 15), (7, 21)]:
             s.record(); hs.detect_multi(red, reqs, status=st, outputs=outs); e.record(); e.synchronize()
             ts.append(s.elapsed_time(e))
         res[kappa] = (sorted(ts)[2], [o[0].clone() for o in outs])
-    diff = [int((a != b).sum()) for a, b in zip(res["1e4"][1], res["0"][1])]
-    print(f"{inner}/{outer}: repair on {res['1e4'][0]:.3f} ms, off {res['0'][0]:.3f} ms, "
+    diff = [int((a != b).sum()) for a, b in zip(res["on"][1], res["off"][1])]
+    print(f"{inner}/{outer}: repair on {res['on'][0]:.3f} ms, off {res['off'][0]:.3f} ms, "
           f"pixels changed by the repair lrx/dwrx/dwest {diff}", flush=True)
