@@ -17,9 +17,10 @@ One step = one pass of that hot path over the cube:
           three streams, so the kernels and the D2H overlap the PCIe H2D).
 Multi-GPU (torchrun): row strips aligned to hsad_row_quantum, each rank holds its
 strip + mirror halo (generated from the same seeded row chunks = the host copy),
-computes it, and the maps are gathered to rank 0 with NCCL (asynchronous dist.gather
-per window-pair group, so a group's maps travel while the next group's detectors run;
-sharded.MapGather) inside the timed region. scaling = "strong" (the 4096^2 image is fixed).
+computes it, and the maps are gathered to rank 0 with NCCL through the product's C-ABI
+(hsad_gather_maps: grouped ncclSend / ncclRecv straight into rank 0's full maps, one per
+map, on a gather stream, so a window-pair group's maps travel while the next group's
+detectors run; sharded.NcclMapGather) inside the timed region. scaling = "strong" (the 4096^2 image is fixed).
 
 --impl reference times the CPU restatement of the reference (oracle/, the
 reference itself needs Eigen3, absent here) on the host cores, rank 0 only.
@@ -372,10 +373,16 @@ def detector_ncu():
         except (KeyError, TypeError, ValueError):
             return None
         return round(f * 1.965e9 / 1e12, 2)
+    peak_file = ROOT / "profiles" / "fp64_peak_r2.json"
+    try:
+        fp64_peak = json.loads(peak_file.read_text())["dfma_tflops"]
+        peak_src = f"{peak_file.relative_to(ROOT)} (harness/peaks/fp64_peak.cu on a B200)"
+    except Exception:
+        fp64_peak, peak_src = None, "profiles/fp64_peak_r2.json missing"
     return {"ncu_issue_active_frac": [round(float(k[key_i]) / 100, 3) for k in det],
             "ncu_fp64_pipe_frac": [round(float(k[key_f]) / 100, 3) for k in det],
             "ncu_fp64_tflops_executed": [fp64_tflops(k) for k in det],
-            "fp64_peak_tflops_measured": 35.4,
+            "fp64_peak_tflops_measured": fp64_peak, "fp64_peak_source": peak_src,
             "ncu_source": "profiles/ncu_full_r1_sweep_d.json (fast passes of the 7/3, 11/5, 15/5, 21/7 detectors)"}
 
 
@@ -406,6 +413,9 @@ def main():
     cfg = CONFIGS[args.config]
     dist = None
     if world > 1:
+        # the communicator set-up lines ("... nranks N ...") show the rank count in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         if args.impl == "b200":  # the reference arm is CPU-only (gloo)
             torch.cuda.set_device(local)
@@ -440,8 +450,12 @@ def run_b200(args, cfg, rank, world, local, dist):
     red = torch.empty((nb, samples, 4), dtype=torch.float64, device=dev)
     # maps live in padded (per, samples) buffers: the strip's rows come first, so at N > 1
     # they are the NCCL send buffers themselves (no staging copy)
-    from paper_1201_2025_b200.sharded import MapGather
-    gather = MapGather(plan, dist) if world > 1 else None
+    from paper_1201_2025_b200.sharded import MapGather, NcclMapGather
+    # the product's C-ABI NCCL gather (hsad_gather_maps) on its own communicator;
+    # HSAD_TORCH_GATHER=1 uses torch.distributed.gather instead
+    gather = None
+    if world > 1:
+        gather = MapGather(plan, dist) if os.environ.get("HSAD_TORCH_GATHER") else NcclMapGather(plan, dist)
     pad = lambda dt: torch.zeros((max(per, r1 - r0), samples), dtype=dt, device=dev)  # noqa: E731
     outs_pad = [(pad(torch.float64), pad(torch.int8) if r.eigcount else None) for r in reqs]
     outs = [(sc[: r1 - r0], None if cnt is None else cnt[: r1 - r0]) for sc, cnt in outs_pad]
@@ -473,10 +487,11 @@ def run_b200(args, cfg, rank, world, local, dist):
                                        len(idx), status.data_ptr(), None, stream.cuda_stream)
             assert st == 0, lib.hsad_last_error_message()
             if gather is not None:  # NCCL gather of this group's maps, overlapping the next group
+                src = outs_pad if isinstance(gather, MapGather) else outs
                 for i in idx:
-                    gather.launch(2 * i, outs_pad[i][0])
-                    if outs_pad[i][1] is not None:
-                        gather.launch(2 * i + 1, outs_pad[i][1])
+                    gather.launch(2 * i, src[i][0])
+                    if src[i][1] is not None:
+                        gather.launch(2 * i + 1, src[i][1])
         if record:
             ev[2].record(stream)
         if gather is not None:

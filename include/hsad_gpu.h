@@ -85,7 +85,8 @@ typedef enum hsad_status {
     HSAD_E_IO_FAILURE = 21,
     /* B200 path only */
     HSAD_E_CUDA = 64,        /* no device / launch or runtime failure */
-    HSAD_E_UNSUPPORTED = 65  /* outside this build's kernel limits (see hsad_limits) */
+    HSAD_E_UNSUPPORTED = 65, /* outside this build's kernel limits (see hsad_limits) */
+    HSAD_E_NCCL = 66         /* NCCL missing or an NCCL call failed (hsad_gather_maps) */
 } hsad_status;
 
 typedef enum hsad_algorithm { /* hsad::Algorithm, detect.hpp:13 */
@@ -218,15 +219,47 @@ hsad_status hsad_pipeline_host(const float* h_cube, int64_t lines, int64_t sampl
                                hsad_pixel_error* err, void* stream);
 
 /* One process, G GPUs: the image splits into n_strips row strips aligned to
- * hsad_row_quantum; strip g runs on device g % deviceCount from its own host thread
- * (buffer rows = strip + reflected window halo from h_cube, reduce, fused detectors on
- * the strip's rows) and writes its map rows straight into the HOST maps of host_requests.
- * Maps are bit-identical to a one-strip run. Errors: the first failing pixel in row-major
- * order, as one sequential call would report it. Synchronous. */
+ * hsad_row_quantum (hsad_strip_plan), dealt to the devices in contiguous blocks; a host
+ * thread per device streams its row range like hsad_pipeline_host (buffer rows = range +
+ * reflected window halo from h_cube, H2D overlapped with reduce, fused detectors and the
+ * D2H of finished rows, on the device's persistent buffers and streams) and writes its
+ * map rows straight into the HOST maps of host_requests. Maps are bit-identical to a
+ * one-strip run. Errors: the first failing request at its first failing pixel, as one
+ * sequential call would report it. Synchronous. */
 hsad_status hsad_pipeline_sharded(const float* h_cube, int64_t lines, int64_t samples, int32_t bands,
                                   int32_t order, int32_t target_bands,
                                   const hsad_detect_request* host_requests, int32_t n_requests,
                                   int32_t n_strips, hsad_pixel_error* err);
+
+/* ---- multi-GPU row strips and the NCCL score-map gather ----------------- */
+/* Rank `rank` of `world` owns output rows [*row0, *row1): strips of *strip_rows rows, a
+ * multiple of hsad_row_quantum (so every map is bit-identical to a one-GPU run). The
+ * reference's analogue is parallel_rows' row split, proj/core/src/parallel.hpp:17-40. */
+hsad_status hsad_strip_plan(int64_t lines, int64_t samples, int32_t world, int32_t rank,
+                            int64_t* row0, int64_t* row1, int64_t* strip_rows);
+
+typedef struct hsad_map_desc {
+    const void* d_strip;   /* this rank's rows [row0, row1) x samples (device) */
+    void* d_full;          /* root only: the lines x samples map (device); may hold d_strip */
+    int32_t elem_bytes;    /* 8 fp64 scores, 4 fp32 scores, 1 int8 DWEST eigen-counts */
+} hsad_map_desc;
+
+/* Gathers every rank's strip of each map into the root's full maps: one grouped
+ * ncclSend per map on the other ranks, ncclRecv straight into place on the root (strips
+ * are contiguous row blocks), a device copy for the root's own strip. nccl_comm is the
+ * caller's ncclComm_t over `world` ranks (ncclCommInitRank / hsad_nccl_comm_init_*);
+ * single-process multi-GPU callers issue one call per device from one host thread per
+ * device. Enqueued on `stream`; NCCL is loaded at run time (libnccl.so.2). */
+hsad_status hsad_gather_maps(void* nccl_comm, int32_t world, int32_t rank, int32_t root,
+                             int64_t lines, int64_t samples, const hsad_map_desc* maps,
+                             int32_t n_maps, void* stream);
+/* Communicator helpers for callers without their own NCCL setup (thin wrappers of
+ * ncclGetUniqueId / ncclCommInitRank / ncclCommInitAll / ncclCommDestroy). */
+hsad_status hsad_nccl_available(void);
+hsad_status hsad_nccl_unique_id(uint8_t* id128);
+hsad_status hsad_nccl_comm_init_rank(void** comm, int32_t world, const uint8_t* id128, int32_t rank);
+hsad_status hsad_nccl_comm_init_all(void** comms, int32_t ndev);
+hsad_status hsad_nccl_comm_destroy(void* comm);
 
 /* ---- ENVI ingest --------------------------------------------- */
 typedef enum hsad_interleave { /* hsad::Interleave, cube.hpp:20 */

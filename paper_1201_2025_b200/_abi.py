@@ -28,6 +28,7 @@ HSAD_E_DIMENSION_MISMATCH = 19
 HSAD_E_DEGENERATE_TRUTH = 20
 HSAD_E_CUDA = 64
 HSAD_E_UNSUPPORTED = 65
+HSAD_E_NCCL = 66
 
 HSAD_LRX, HSAD_DWRX, HSAD_DWEST = 0, 1, 2
 WINDOW_SINGLE, WINDOW_DUAL = 0, 1
@@ -39,6 +40,8 @@ EXPORTED = [
     "hsad_reduce", "hsad_detect", "hsad_detect_multi", "hsad_strip_rows", "hsad_row_quantum",
     "hsad_decode_status", "hsad_pipeline_host", "hsad_reduce_detect",
     "hsad_read_cube", "hsad_reduce_raw", "hsad_pipeline_raw", "hsad_pipeline_sharded", "hsad_roc", "hsad_top_k", "hsad_adaptive_threshold", "hsad_render_pgm",
+    "hsad_strip_plan", "hsad_gather_maps", "hsad_nccl_available", "hsad_nccl_unique_id",
+    "hsad_nccl_comm_init_rank", "hsad_nccl_comm_init_all", "hsad_nccl_comm_destroy",
 ]
 
 HSAD_BSQ, HSAD_BIL, HSAD_BIP = 0, 1, 2
@@ -68,6 +71,10 @@ class CubeHeader(C.Structure):  # hsad_cube_header
 class RocSummary(C.Structure):  # hsad_roc_summary
     _fields_ = [("positives", C.c_uint64), ("negatives", C.c_uint64),
                 ("auc_twice_num", C.c_uint64), ("auc", C.c_double), ("distinct", C.c_uint64)]
+
+
+class MapDesc(C.Structure):  # hsad_map_desc
+    _fields_ = [("d_strip", C.c_void_p), ("d_full", C.c_void_p), ("elem_bytes", C.c_int32)]
 
 
 class Limits(C.Structure):
@@ -114,6 +121,13 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
         "hsad_top_k": (I32, [VP, I32, I64, I64, VP, P(D), VP]),
         "hsad_adaptive_threshold": (I32, [VP, I32, I64, D, P(D), VP, VP]),
         "hsad_render_pgm": (I32, [VP, I32, I64, VP, VP]),
+        "hsad_strip_plan": (I32, [I64, I64, I32, I32, P(I64), P(I64), P(I64)]),
+        "hsad_gather_maps": (I32, [VP, I32, I32, I32, I64, I64, P(MapDesc), I32, VP]),
+        "hsad_nccl_available": (I32, []),
+        "hsad_nccl_unique_id": (I32, [VP]),
+        "hsad_nccl_comm_init_rank": (I32, [P(VP), I32, VP, I32]),
+        "hsad_nccl_comm_init_all": (I32, [P(VP), I32]),
+        "hsad_nccl_comm_destroy": (I32, [VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

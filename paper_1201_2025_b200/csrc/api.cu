@@ -127,6 +127,7 @@ const char* status_name(int32_t code) {
     if (code >= 0 && code <= HSAD_E_IO_FAILURE) return names[code];
     if (code == HSAD_E_CUDA) return "CudaError";
     if (code == HSAD_E_UNSUPPORTED) return "Unsupported";
+    if (code == HSAD_E_NCCL) return "NcclError";
     return "UnknownError";
 }
 

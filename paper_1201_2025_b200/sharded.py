@@ -39,11 +39,78 @@ class StripPlan:
 
 def plan_strip(lines: int, samples: int, world: int, rank: int,
                requests: Sequence[DetectRequest]) -> StripPlan:
-    q = row_quantum(lines, samples)
-    per = -(-lines // (world * q)) * q
-    r0, r1 = min(lines, rank * per), min(lines, (rank + 1) * per)
+    """The C-ABI's strip plan (hsad_strip_plan, the split hsad_gather_maps and
+    hsad_pipeline_sharded use) plus the strip's buffer rows (hsad_strip_rows)."""
+    import ctypes as C
+    from . import _abi
+    from .hsad import _check
+    r0, r1, per = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(_abi.lib().hsad_strip_plan(lines, samples, world, rank, C.byref(r0), C.byref(r1),
+                                      C.byref(per)))
+    r0, r1 = r0.value, r1.value
     b0, nb = strip_rows(lines, r0, r1, requests) if r1 > r0 else (r0, 0)
-    return StripPlan(lines, samples, world, rank, q, per, r0, r1, b0, nb)
+    return StripPlan(lines, samples, world, rank, row_quantum(lines, samples), per.value, r0, r1,
+                     b0, nb)
+
+
+class NcclMapGather:
+    """Score-map gather to rank `dst` through the C-ABI (hsad_gather_maps: grouped
+    ncclSend / ncclRecv straight into the root's full maps) on an NCCL communicator the
+    library creates from a unique id broadcast over `dist` (any backend).
+
+    launch(slot, strip) enqueues one map's gather on the current stream; full(slot) is the
+    root's (lines, samples) map, allocated once per slot and reused across calls."""
+
+    def __init__(self, plan: StripPlan, dist, dst: int = 0):
+        import ctypes as C
+        from . import _abi
+        from .hsad import _check
+        self.plan, self.dst, self._C, self._abi = plan, dst, C, _abi
+        self.full_maps: dict[int, torch.Tensor] = {}
+        self.stream = None
+        self.comm = C.c_void_p()
+        if plan.world > 1:
+            uid = (C.c_uint8 * 128)()
+            if plan.rank == 0:
+                _check(_abi.lib().hsad_nccl_unique_id(uid))
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend() == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=0)
+            uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+            _check(_abi.lib().hsad_nccl_comm_init_rank(C.byref(self.comm), plan.world, uid, plan.rank))
+
+    def launch(self, slot: int, strip: torch.Tensor) -> None:
+        """Enqueues the gather of `strip` on the gather stream once the current stream's
+        work so far (the kernels that wrote it) is done: it overlaps the next kernels."""
+        from .hsad import _check
+        p = self.plan
+        if self.stream is None:
+            self.stream = torch.cuda.Stream(device=strip.device)
+        self.stream.wait_stream(torch.cuda.current_stream(strip.device))
+        full = None
+        if p.rank == self.dst:
+            full = self.full_maps.get(slot)
+            if full is None:
+                full = torch.empty((p.lines, p.samples), dtype=strip.dtype, device=strip.device)
+                self.full_maps[slot] = full
+        desc = (self._abi.MapDesc * 1)(self._abi.MapDesc(
+            strip.data_ptr(), full.data_ptr() if full is not None else None, strip.element_size()))
+        _check(self._abi.lib().hsad_gather_maps(self.comm, p.world, p.rank, self.dst, p.lines,
+                                                p.samples, desc, 1, self.stream.cuda_stream))
+
+    def wait(self) -> None:
+        """The current stream waits for every gather launched so far."""
+        if self.stream is not None:
+            torch.cuda.current_stream(self.stream.device).wait_stream(self.stream)
+
+    def full(self, slot: int) -> torch.Tensor | None:
+        return self.full_maps.get(slot) if self.plan.rank == self.dst else None
+
+    def close(self) -> None:
+        if self.comm.value:
+            self._abi.lib().hsad_nccl_comm_destroy(self.comm)
+            self.comm = self._C.c_void_p()
 
 
 def compute_strip_gpu(buf: torch.Tensor, plan: StripPlan, requests: Sequence[DetectRequest],
@@ -133,9 +200,10 @@ def run_sharded(rows_of: Callable[[int, int], torch.Tensor], lines: int, samples
 
 def pipeline_sharded(h_cube: torch.Tensor, order: int, target_bands: int,
                      requests: Sequence[DetectRequest], outputs, n_strips: int):
-    """hsad_pipeline_sharded: one process, n_strips row strips over the visible GPUs
-    (strip g on device g % count), host fp32 BIP cube in, host maps out (each GPU writes
-    its own rows; no collective). `outputs`: (scores, eigcount-or-None) CPU tensors."""
+    """hsad_pipeline_sharded: one process, n_strips row strips dealt in contiguous blocks
+    to the visible GPUs, host fp32 BIP cube in, host maps out (each GPU streams its own
+    rows like hsad_pipeline_host; no collective). `outputs`: (scores, eigcount-or-None)
+    CPU tensors."""
     import ctypes as C
     from . import _abi
     from .hsad import _check, _make_request

@@ -12,5 +12,5 @@ mkdir -p "$ROOT/variants/obj_$name"
 SRC=${SRC:-detect}
 objs=$(ls "$ROOT"/paper_1201_2025_b200/build/*.o | grep -v "/$SRC.o$")
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared \
-  -o "$ROOT/variants/$name.so" "$ROOT/variants/obj_$name/${SRC:-detect}.o" $objs
+  -o "$ROOT/variants/$name.so" "$ROOT/variants/obj_$name/${SRC:-detect}.o" $objs -Xcompiler -pthread -ldl
 echo "built variants/$name.so"

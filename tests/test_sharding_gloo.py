@@ -180,3 +180,18 @@ def test_grouped_async_gather_like_bench(orc, world):
     for m, w in zip(got[:4], want):
         assert np.array_equal(m, w)
     assert np.array_equal(got[4], counts[0]) and np.array_equal(got[5], counts[1])
+
+
+def test_strip_plan_tiles_the_image():
+    """hsad_strip_plan (the split hsad_gather_maps, hsad_pipeline_sharded and the bench
+    use): strips are contiguous, quantum-aligned and tile [0, lines) for any world size."""
+    from paper_1201_2025_b200.hsad import row_quantum
+    from paper_1201_2025_b200.sharded import plan_strip
+    for lines, samples in ((4096, 4096), (512, 614), (37, 23), (100, 100), (5, 7)):
+        q = row_quantum(lines, samples)
+        for world in (1, 2, 3, 4, 8):
+            plans = [plan_strip(lines, samples, world, r, []) for r in range(world)]
+            assert plans[0].r0 == 0 and plans[-1].r1 == lines
+            for a, b in zip(plans, plans[1:]):
+                assert a.r1 == b.r0
+            assert all(p.r0 % q == 0 and p.per % q == 0 for p in plans if p.r1 > p.r0)
