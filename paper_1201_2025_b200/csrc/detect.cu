@@ -52,6 +52,7 @@ __device__ unsigned long long g_phase_cycles[8];
 namespace hsad_b200 {
 
 hsad_status fullband_launch(FbParams& P, cudaStream_t s);
+hsad_status fullband_dwest_launch(FbParams& P, cudaStream_t s);
 
 namespace {
 
@@ -1477,14 +1478,6 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     // bands > 8: the full-band path (K5/K6, fullband.cu) for LRX / DWRX
     const bool fullband = bands > kMaxDetectBands;
     if (bands < 1) return set_error(HSAD_E_INVALID_VALUE, "cube has no bands");
-    if (fullband)
-        for (int q = 0; q < n_requests; ++q)
-            if (requests[q].algorithm == HSAD_DWEST)
-                return set_error(HSAD_E_UNSUPPORTED,
-                                 "full-band DWEST (" + std::to_string(bands) +
-                                     " bands) is not in this build; reduce the cube first "
-                                     "(hsad_reduce) or use <= " +
-                                     std::to_string(kMaxDetectBands) + " bands");
     if (lines < 0 || samples < 0 || row_begin < 0 || row_end > lines || row_begin > row_end)
         return set_error(HSAD_E_INVALID_VALUE, "row range outside the image");
     if (row_begin == row_end || samples == 0) return HSAD_OK;
@@ -1595,14 +1588,19 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             F.outer = R.algorithm == HSAD_LRX ? R.window.single_size : R.window.outer_size;
             F.inner = R.algorithm == HSAD_LRX ? (R.guard <= 0 ? 1 : R.guard) : R.window.inner_size;
             F.ridge = R.ridge;
+            F.frac = R.eigen_fraction;
             F.scores = scratch ? static_cast<void*>(scratch + scratch_stride * q)
                                : R.d_scores;
+            F.eigcount = R.algorithm != HSAD_DWEST || !R.d_eigcount ? nullptr
+                         : scratch ? reinterpret_cast<int8_t*>(scratch + scratch_stride * q +
+                                                               static_cast<size_t>(samples) * 8)
+                                   : R.d_eigcount;
             F.score_bytes = R.score_bytes;
             F.status = status;
             F.req = req_base + q;
             F.diag_lin = req_base + q == diag_req ? diag_lin : -1;
             F.diag_out = diag_out;
-            hsad_status fst = fullband_launch(F, s);
+            hsad_status fst = R.algorithm == HSAD_DWEST ? fullband_dwest_launch(F, s) : fullband_launch(F, s);
             if (fst != HSAD_OK) return fst;
         }
         return HSAD_OK;
@@ -1630,6 +1628,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         std::string msg;
         if (overflow) {
             msg = "inverse overflowed";
+        } else if (code == HSAD_E_UNSUPPORTED) {
+            msg = "more than 16 eigenvectors pass the DWEST cutoff (full-band kernel limit)";
         } else {
             // re-run the failing row to recover that pixel's ridge for the message
             double delta = 0.0;

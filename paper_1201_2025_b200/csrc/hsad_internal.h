@@ -115,7 +115,7 @@ struct FbParams {
     int bands;
     int64_t buf_row0;
     int64_t row_begin, row_end;
-    int algo;           // HSAD_LRX or HSAD_DWRX
+    int algo;           // HSAD_LRX, HSAD_DWRX or HSAD_DWEST
     int outer;          // LRX window / DWRX outer
     int inner;          // LRX guard (1 = centre only) / DWRX inner
     double ridge;
@@ -125,6 +125,8 @@ struct FbParams {
     int req;            // position of the request in the call (failure ordering)
     int64_t diag_lin;
     double* diag_out;
+    double frac;        // DWEST eigen fraction
+    int8_t* eigcount;   // DWEST eigen-count map (nullable)
     int chunk;          // samples per shared-memory chunk (set by fullband_launch)
     int mp;             // bordered dimension L+1 rounded up to a multiple of 4
 };

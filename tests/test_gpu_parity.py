@@ -364,11 +364,49 @@ def test_fullband_config_c3(orc):
                      lambda r, c: orc.port.hp_dwrx(ch, 5, 15, r, c, workers=16)[0], "C3 dwrx 5/15")
 
 
-def test_fullband_dwest_unsupported_and_errors(orc):
-    cube = gpu(orc.port.random_cube(6, 6, 20, 3))
+def _dwest_full_check(orc, cube, inner, outer, rows=None, frac=0.1, what=""):
+    """Full-band DWEST (fullband_dwest.cu) against the oracle (cyclic Jacobi to fp64,
+    hsad_oracle.cpp): scores within 1e-9, identical eigen-counts; pixels whose DWEST
+    decision margins (oracle.port.dwest_margins) are below 1e-10 are hazards (SURVEY
+    App. A.7) and may legitimately differ — they are counted, and must be rare."""
+    (e, n), = run(cube, [hs.DetectRequest("dwest", W2(inner, outer), eigen_fraction=frac, eigcount=True)])
+    rb, re = rows if rows else (0, cube.shape[0])
+    s, c = orc.port.dwest(cube, inner, outer, frac, workers=16, rows=(rb, re))
+    cm, sm_ = orc.port.dwest_margins(cube, inner, outer, frac, workers=16, rows=(rb, re))
+    hazard = (cm < 1e-10) | (sm_ < 1e-10)
+    e, n = e[rb:re], n[rb:re]
+    err = np.abs(e - s) / np.maximum(1.0, np.maximum(np.abs(e), np.abs(s)))
+    assert np.all(err[~hazard] <= TOL64), f"{what}: max {err[~hazard].max():.3g}"
+    assert np.array_equal(n[~hazard], c[~hazard]), f"{what}: eigen-counts"
+    assert hazard.sum() <= max(1, hazard.size // 1000), f"{what}: {int(hazard.sum())} hazard px"
+    return float(err.max()), int(hazard.sum())
+
+
+@pytest.mark.parametrize("bands,inner,outer", [(12, 3, 7), (30, 3, 9), (61, 5, 11), (189, 5, 15)])
+def test_fullband_dwest_random_cubes(orc, bands, inner, outer):
+    cube = orc.port.random_cube(9, 11, bands, 700 + bands)
+    _dwest_full_check(orc, cube, inner, outer, what=f"dwest L={bands}")
+
+
+def test_fullband_dwest_config_c3(orc):
+    """DWEST on the raw 189-band C3 cube (BASELINE configs[2] geometry, 5/15 windows):
+    the reference's acceptance criterion 7 runs DWEST without a DWT (proj/tests/acceptance/
+    acceptance_main.cpp:305-309). Border rows and interior rows against the oracle."""
+    cfg = CONFIGS["C3"]
+    cube, _ = generate_scene(cfg["lines"], cfg["samples"], cfg["bands"], cfg["seed"], cfg["rate"])
+    ch = cube.numpy()
+    for rows in ((0, 3), (48, 51), (97, 100)):
+        _dwest_full_check(orc, ch, 5, 15, rows=rows, what=f"C3 dwest rows {rows}")
+
+
+def test_fullband_dwest_limits_and_errors(orc):
+    cube = gpu(orc.port.random_cube(4, 5, 208, 3))
     with pytest.raises(hs.HsadError) as e:
         hs.dwest(cube, W2(3, 5))
     assert e.value.name == "Unsupported"
+    with pytest.raises(hs.HsadError) as e:
+        hs.dwest(gpu(orc.port.random_cube(6, 6, 20, 3)), W2(1, 5))
+    assert e.value.name == "TooFewSamples" and "at pixel (0, 0)" in str(e.value)
     flat = np.zeros((5, 5, 12)); flat[2, 2] = 1.0
     with pytest.raises(OracleError) as want:
         orc.port.local_rx(flat, 3, 1e-6)
