@@ -1629,7 +1629,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         if (overflow) {
             msg = "inverse overflowed";
         } else if (code == HSAD_E_UNSUPPORTED) {
-            msg = "more than 16 eigenvectors pass the DWEST cutoff (full-band kernel limit)";
+            msg = "more than 64 eigenvectors pass the DWEST cutoff (full-band kernel limit)";
         } else {
             // re-run the failing row to recover that pixel's ridge for the message
             double delta = 0.0;

@@ -31,7 +31,8 @@ namespace hsad_b200 {
 
 constexpr int kDwThreads = 256;
 constexpr int kDwMaxBands = 200;
-constexpr int kDwMaxSel = 16;    // selected eigenvectors per pixel (f = 0.1 selects 1-3)
+constexpr int kDwMaxSel = 64;    // selected eigenvectors per pixel (<= inner^2 - 1; scenes: 1-3)
+constexpr int kDwRing = 16;      // eigenvectors kept for re-orthogonalisation within clusters
 constexpr int kDwMaxTiles = 5;   // 4x4 Gram tiles per thread (lower triangle of 200 x 200)
 
 namespace {
@@ -335,49 +336,55 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
     }
     __syncthreads();
 
-    // 5. eigenvectors of T (twisted factorisation), one at a time by warp 0 lane 0;
-    // z_j lives in xs[j * L4 ...] (the Gram stage is finished)
-    double* lft = vv;  // [L4] l_i of T - lambda I = L D L^T
-    double* dpl = xs + static_cast<int64_t>(kDwMaxSel) * L4;  // [L4] stationary pivots d+
-    double* upr = dpl + L4;                                    // [L4] u_i of U D U^T
+    // 5./6. one selected eigenvector at a time, in descending eigenvalue order:
+    //   a. lane 0 of warp 0: eigenvector z of T (twisted factorisation) into a ring of the
+    //      last kDwRing vectors kept in the tridiagonal basis;
+    //   b. CTA: re-orthogonalise z against the ring vectors of the same cluster, normalise;
+    //   c. warp 0: back-transformation v = H_0 ... H_{n-3} z (reflectors in A's columns),
+    //      the sign rule (first largest-|.| component positive) and v . m_diff.
+    // The xs region (the Gram's sample stage) holds the ring, v and two pivot vectors.
+    double* ring = xs;                                         // [kDwRing][L4]
+    double* vw = xs + static_cast<int64_t>(kDwRing) * L4;      // [L4] vector being transformed
+    double* dpl = vw + L4;                                     // [L4] stationary pivots d+
+    double* dmi = dpl + L4;                                    // [L4] progressive pivots d-
     for (int j = 0; j < nsel; ++j) {
-        double* z = xs + static_cast<int64_t>(j) * L4;
+        double* z = ring + static_cast<int64_t>(j % kDwRing) * L4;
         if (t == 0) {
             const double lj = lam[j];
+            // T - lambda I = L D+ L^T (top down) and U D- U^T (bottom up)
             double dp = dg[0] - lj;
             for (int i = 0; i < L - 1; ++i) {
                 if (fabs(dp) < pivmin) dp = -pivmin;
                 dpl[i] = dp;
-                lft[i] = ev[i] / dp;
-                dp = (dg[i + 1] - lj) - lft[i] * ev[i];
+                dp = (dg[i + 1] - lj) - ev[i] / dp * ev[i];
             }
             if (fabs(dp) < pivmin) dp = -pivmin;
             dpl[L - 1] = dp;
-            // progressive U D U^T from the bottom; twist index at the smallest |gamma|
             double dm = dg[L - 1] - lj;
             if (fabs(dm) < pivmin) dm = -pivmin;
+            dmi[L - 1] = dm;
             int tw = L - 1;
             double gbest = fabs(dpl[L - 1]);  // gamma_{n-1} = d+_{n-1}
             for (int i = L - 2; i >= 0; --i) {
-                upr[i] = ev[i] / dm;
-                dm = (dg[i] - lj) - upr[i] * ev[i];
+                dm = (dg[i] - lj) - ev[i] / dm * ev[i];
                 if (fabs(dm) < pivmin) dm = -pivmin;
-                const double gam = dpl[i] + dm - (dg[i] - lj);
+                dmi[i] = dm;
+                const double gam = dpl[i] + dm - (dg[i] - lj);  // twist at i
                 if (fabs(gam) < gbest) {
                     gbest = fabs(gam);
                     tw = i;
                 }
             }
+            // z_tw = 1; L^T rows above the twist, U^T rows below it
             z[tw] = 1.0;
-            for (int i = tw - 1; i >= 0; --i) z[i] = -lft[i] * z[i + 1];
-            for (int i = tw; i < L - 1; ++i) z[i + 1] = -upr[i] * z[i];
+            for (int i = tw - 1; i >= 0; --i) z[i] = -(ev[i] / dpl[i]) * z[i + 1];
+            for (int i = tw; i < L - 1; ++i) z[i + 1] = -(ev[i] / dmi[i + 1]) * z[i];
             for (int i = L; i < L4; ++i) z[i] = 0.0;
         }
         __syncthreads();
-        // normalise; re-orthogonalise against earlier vectors of the same cluster
-        for (int q = 0; q < j; ++q) {
-            if (fabs(lam[q] - lam[j]) > 1e-3 * tnorm) continue;  // uniform
-            const double* zq = xs + static_cast<int64_t>(q) * L4;
+        for (int q = j - 1; q >= 0 && q > j - kDwRing; --q) {
+            if (fabs(lam[q] - lam[j]) > 1e-3 * tnorm) break;  // clusters are contiguous
+            const double* zq = ring + static_cast<int64_t>(q % kDwRing) * L4;
             double part = 0.0;
             for (int i = t; i < L; i += kDwThreads) part = fma(zq[i], z[i], part);
             const double dot = block_sum(part, red);
@@ -387,47 +394,46 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
         double part = 0.0;
         for (int i = t; i < L; i += kDwThreads) part = fma(z[i], z[i], part);
         const double inv = 1.0 / sqrt(block_sum(part, red));
-        for (int i = t; i < L; i += kDwThreads) z[i] *= inv;
+        for (int i = t; i < L4; i += kDwThreads) {
+            z[i] *= inv;
+            vw[i] = z[i];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            for (int k = L - 3; k >= 0; --k) {
+                const double b = bet[k];
+                if (b == 0.0) continue;
+                double s2 = 0.0;
+                for (int i = k + 1 + lane; i < L; i += 32) s2 = fma(A[pk(i, k)], vw[i], s2);
+                for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+                const double f = b * s2;
+                for (int i = k + 1 + lane; i < L; i += 32) vw[i] = fma(-f, A[pk(i, k)], vw[i]);
+                __syncwarp();
+            }
+            // first index of the largest |component| (stats.cpp:83-85), then v . m
+            double best = -1.0, dot = 0.0;
+            int bidx = L;
+            for (int i = lane; i < L; i += 32) {
+                const double a = fabs(vw[i]);
+                if (a > best) {
+                    best = a;
+                    bidx = i;
+                }
+                dot = fma(vw[i], mu_in[i], dot);
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+                if (ob > best || (ob == best && oi < bidx)) {
+                    best = ob;
+                    bidx = oi;
+                }
+                dot += __shfl_xor_sync(0xffffffffu, dot, off);
+            }
+            if (lane == 0) contrib[j] = vw[bidx] < 0.0 ? -dot : dot;
+        }
         __syncthreads();
     }
-
-    // 6. back-transformation v = H_0 ... H_{n-3} z (one warp per vector), sign rule,
-    // projection on m_diff
-    for (int j = warp; j < nsel; j += kDwThreads / 32) {
-        double* z = xs + static_cast<int64_t>(j) * L4;
-        for (int k = L - 3; k >= 0; --k) {
-            const double b = bet[k];
-            if (b == 0.0) continue;
-            double s = 0.0;
-            for (int i = k + 1 + lane; i < L; i += 32) s = fma(A[pk(i, k)], z[i], s);
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            const double f = b * s;
-            for (int i = k + 1 + lane; i < L; i += 32) z[i] = fma(-f, A[pk(i, k)], z[i]);
-            __syncwarp();
-        }
-        // first index of the largest |component| (stats.cpp:83-85), then v . m
-        double best = -1.0, dot = 0.0;
-        int bidx = L;
-        for (int i = lane; i < L; i += 32) {
-            const double a = fabs(z[i]);
-            if (a > best) {
-                best = a;
-                bidx = i;
-            }
-            dot = fma(z[i], mu_in[i], dot);
-        }
-        for (int off = 16; off > 0; off >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-            const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
-            if (ob > best || (ob == best && oi < bidx)) {
-                best = ob;
-                bidx = oi;
-            }
-            dot += __shfl_xor_sync(0xffffffffu, dot, off);
-        }
-        if (lane == 0) contrib[j] = z[bidx] < 0.0 ? -dot : dot;
-    }
-    __syncthreads();
     if (t == 0) {
         double proj = 0.0;
         for (int j = 0; j < nsel; ++j) proj += contrib[j];  // descending eigenvalue order
@@ -449,13 +455,13 @@ hsad_status fullband_dwest_launch(FbParams& P, cudaStream_t s) {
     const int64_t tri = static_cast<int64_t>(L4) * (L4 + 1) / 2;
     const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;
     auto bytes = [&](int ch) {
-        // xs must also hold kDwMaxSel vectors + 2 work vectors after the Gram
-        const int64_t xs = static_cast<int64_t>(ch > kDwMaxSel + 2 ? ch : kDwMaxSel + 2) * L4;
+        // xs must also hold the ring + 3 work vectors after the Gram
+        const int64_t xs = static_cast<int64_t>(ch > kDwRing + 3 ? ch : kDwRing + 3) * L4;
         return (tri + xs + 7 * static_cast<int64_t>(L4) + 64 + 2 * kDwMaxSel + nsamp) * 8;
     };
     int chunk = 32;
-    while (chunk > kDwMaxSel + 2 && bytes(chunk) > 227 * 1024) chunk /= 2;
-    if (chunk < kDwMaxSel + 2) chunk = kDwMaxSel + 2;
+    while (chunk > kDwRing + 3 && bytes(chunk) > 227 * 1024) chunk /= 2;
+    if (chunk < kDwRing + 3) chunk = kDwRing + 3;
     if (bytes(chunk) > 227 * 1024)
         return set_error(HSAD_E_UNSUPPORTED, "full-band DWEST working set exceeds shared memory");
     P.chunk = chunk;
