@@ -131,6 +131,12 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
     int64_t* base = reinterpret_cast<int64_t*>(contrib + kDwMaxSel);  // [outer^2] offsets
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#ifdef HSAD_DW_DEBUG
+    long long dbg_t0 = clock64(), dbg_ph[8] = {0};
+#define DW_MARK(i) do { long long t1_ = clock64(); dbg_ph[i] += t1_ - dbg_t0; dbg_t0 = t1_; } while (0)
+#else
+#define DW_MARK(i) do { } while (0)
+#endif
     const int c = blockIdx.x;
     const int64_t r = P.row_begin + blockIdx.y;
     if (r >= P.row_end) return;
@@ -227,6 +233,7 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
     }
     for (int b = t; b < L4; b += kDwThreads) mu_in[b] = mu_in[b] - mu_an[b];  // m_diff
     __syncthreads();
+    DW_MARK(0);
 
     // 3. Householder tridiagonalisation (lower): reflector k zeroes A(k+2.., k)
     for (int k = 0; k + 2 < L; ++k) {
@@ -253,13 +260,30 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
             __syncthreads();
             continue;
         }
-        // p = b A_trail v (symmetric, lower packed)
-        for (int i = k + 1 + t; i < L; i += kDwThreads) {
-            double s = 0.0;
-            const double* row = A + pk(i, 0);
-            for (int j = k + 1; j <= i; ++j) s = fma(row[j], vv[j], s);
-            for (int j = i + 1; j < L; ++j) s = fma(A[pk(j, i)], vv[j], s);
-            pp[i] = b * s;
+        // p = b A_trail v (symmetric, lower packed): one warp per row, lanes over columns,
+        // four rows per warp in flight (independent accumulators)
+        constexpr int NW = kDwThreads / 32, RU = 4;
+        for (int i0 = k + 1 + warp; i0 < L; i0 += NW * RU) {
+            double s4[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const int i = i0 + u * NW;
+                double acc = 0.0;
+                if (i < L) {
+                    const double* row = A + pk(i, 0);
+                    for (int j = k + 1 + lane; j <= i; j += 32) acc = fma(row[j], vv[j], acc);
+                    for (int j = i + 1 + lane; j < L; j += 32) acc = fma(A[pk(j, i)], vv[j], acc);
+                }
+                s4[u] = acc;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int u = 0; u < RU; ++u) s4[u] += __shfl_xor_sync(0xffffffffu, s4[u], off);
+            if (lane == 0)
+#pragma unroll
+                for (int u = 0; u < RU; ++u)
+                    if (i0 + u * NW < L) pp[i0 + u * NW] = b * s4[u];
         }
         __syncthreads();
         part = 0.0;
@@ -267,21 +291,15 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
         const double K = 0.5 * b * block_sum(part, red);
         for (int i = k + 1 + t; i < L; i += kDwThreads) pp[i] = fma(-K, vv[i], pp[i]);  // w
         __syncthreads();
-        // A_trail -= v w^T + w v^T (lower triangle, rows k+1..L-1)
-        const int m = L - k - 1;
-        const int total = m * (m + 1) / 2;
-        int e = t, ii = 0, jj = t;  // flattened (row ii, column jj <= ii) of the trailing block
-        while (jj > ii) {
-            jj -= ii + 1;
-            ++ii;
-        }
-        for (; e < total; e += kDwThreads) {
-            const int gi = k + 1 + ii, gj = k + 1 + jj;
-            A[pk(gi, gj)] -= fma(vv[gi], pp[gj], pp[gi] * vv[gj]);
-            jj += kDwThreads;
-            while (jj > ii && ii < m) {
-                jj -= ii + 1;
-                ++ii;
+        // A_trail -= v w^T + w v^T (lower triangle): a warp per row, lanes over columns
+        for (int i0 = k + 1 + warp; i0 < L; i0 += NW * RU) {
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const int i = i0 + u * NW;
+                if (i >= L) break;
+                double* row = A + pk(i, 0);
+                const double vi = vv[i], wi = pp[i];
+                for (int j = k + 1 + lane; j <= i; j += 32) row[j] -= fma(vi, pp[j], wi * vv[j]);
             }
         }
         __syncthreads();
@@ -294,6 +312,7 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
         dg[L - 1] = A[pk(L - 1, L - 1)];
     }
     __syncthreads();
+    DW_MARK(1);
     // off-diagonal e_k (sign kept for the vectors) -> squares for the Sturm counts
     double* ev = pp;  // [L4] signed off-diagonal
     for (int i = t; i < L - 1; i += kDwThreads) {
@@ -336,6 +355,7 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
     }
     __syncthreads();
 
+    DW_MARK(2);
     // 5./6. one selected eigenvector at a time, in descending eigenvalue order:
     //   a. lane 0 of warp 0: eigenvector z of T (twisted factorisation) into a ring of the
     //      last kDwRing vectors kept in the tridiagonal basis;
@@ -434,6 +454,12 @@ __global__ void __launch_bounds__(kDwThreads, 1) fullband_dwest_kernel(const FbP
         }
         __syncthreads();
     }
+    DW_MARK(3);
+#ifdef HSAD_DW_DEBUG
+    if (t == 0 && blockIdx.x == 50 && blockIdx.y == 50)
+        printf("dw phases gram %lld tridiag %lld eigvals %lld vectors %lld nsel %d\n", dbg_ph[0], dbg_ph[1],
+               dbg_ph[2], dbg_ph[3], nsel);
+#endif
     if (t == 0) {
         double proj = 0.0;
         for (int j = 0; j < nsel; ++j) proj += contrib[j];  // descending eigenvalue order
