@@ -134,7 +134,7 @@ typedef struct hsad_pixel_error {
 
 /* Kernel limits of this build. */
 typedef struct hsad_limits {
-    int32_t max_detect_bands;   /* bands accepted by hsad_detect* for LRX/DWRX (DWEST: 8) */
+    int32_t max_detect_bands;   /* bands accepted by hsad_detect* for LRX/DWRX (DWEST: 200) */
     int32_t max_window;         /* largest single/outer window edge */
     int32_t max_reduce_bands;   /* bands accepted by hsad_reduce */
 } hsad_limits;

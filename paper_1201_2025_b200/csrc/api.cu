@@ -235,7 +235,7 @@ const char* hsad_last_error_message(void) { return g_last_error.c_str(); }
 
 void hsad_get_limits(hsad_limits* out) {
     if (!out) return;
-    out->max_detect_bands = 224;  // LRX/DWRX full band (fullband.cu); DWEST up to kMaxDetectBands
+    out->max_detect_bands = 224;  // LRX/DWRX full band (fullband.cu); DWEST up to 200 (fullband_dwest.cu)
     out->max_window = 2 * kMaxRadius + 1;
     out->max_reduce_bands = kMaxReduceBands;
 }
