@@ -94,6 +94,8 @@ struct DetectParams {
     int nreq;
     ReqDev req[kMaxRequests];
     int std_layout;  // box 0 = LRX/outer window for every request, box 1 = inner box
+    int trio;        // std layout with exactly one LRX, one DWRX and one DWEST request ...
+    int trio_q[3];   // ... at these request positions (solve_trio interleaves their solves)
     int staged;      // STD kernel: the update rows arrive in shared memory by TMA bulk copies
     unsigned char* zflag;  // per-CTA "saw an all-zero spectrum" (fast pass -> counting pass)
     int has_dual;
@@ -478,15 +480,17 @@ __device__ __forceinline__ void sweep64(double (&a)[L][L], double (&v)[L][L]) {
 //      accumulated into Q.
 // Returns eigenvalues w (diagonal of B) and eigenvectors V (columns), in no
 // particular order: the DWEST selection below does not need them sorted.
-template <int L>
-__device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)[L][L], double (&w)[L]) {
+// Stage 1 (fp32): Jacobi sweeps on the max-normalised matrix -> approximate vectors.
+// UNROLL: the sweeps fully unrolled, so a caller can interleave independent work.
+template <int L, bool UNROLL = false>
+__device__ __forceinline__ void dwest_f32_stage(const double (&A)[L][L], float (&v32)[L][L]) {
     double amax = 0.0;
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
         for (int j = i; j < L; ++j) amax = fmax(amax, fabs(A[i][j]));
     const double scale = amax > 0.0 ? fast_rcp(amax) : 1.0;
-    float a32[L][L], v32[L][L];
+    float a32[L][L];
 #pragma unroll
     for (int i = 0; i < L; ++i)
 #pragma unroll
@@ -504,8 +508,13 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
             vv[j][0] = make_float2(j == 0 ? 1.0f : 0.0f, j == 1 ? 1.0f : 0.0f);
             vv[j][1] = make_float2(j == 2 ? 1.0f : 0.0f, j == 3 ? 1.0f : 0.0f);
         }
+        if constexpr (UNROLL) {
+#pragma unroll
+            for (int sweep = 0; sweep < HSAD_F32_SWEEPS; ++sweep) sweep32_4(a32, vv);
+        } else {
 #pragma unroll 1
-        for (int sweep = 0; sweep < HSAD_F32_SWEEPS; ++sweep) sweep32_4(a32, vv);
+            for (int sweep = 0; sweep < HSAD_F32_SWEEPS; ++sweep) sweep32_4(a32, vv);
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             v32[0][j] = vv[j][0].x;
@@ -517,6 +526,12 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
 #pragma unroll 1
         for (int sweep = 0; sweep < (L <= 4 ? HSAD_F32_SWEEPS : 6); ++sweep) sweep32<L>(a32, v32);
     }
+}
+
+// Stage 2 (fp64): Gram-Schmidt of the fp32 vectors, B = Q^T A Q, polish sweeps.
+template <int L>
+__device__ __forceinline__ void dwest_f64_stage(const double (&A)[L][L], const float (&v32)[L][L],
+                                                double (&V)[L][L], double (&w)[L]) {
     // modified Gram-Schmidt in fp64
 #pragma unroll
     for (int j = 0; j < L; ++j) {
@@ -581,6 +596,13 @@ __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)
     }
 #pragma unroll
     for (int i = 0; i < L; ++i) w[i] = B[i][i];
+}
+
+template <int L>
+__device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)[L][L], double (&w)[L]) {
+    float v32[L][L];
+    dwest_f32_stage<L>(A, v32);
+    dwest_f64_stage<L>(A, v32, V, w);
 }
 
 __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s) {
@@ -780,9 +802,17 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const R
 
 // DWEST (detect.cpp:242-271)
 template <int L>
+__device__ __forceinline__ void dwest_select(const ReqDev& R, const DualStats<L>& D,
+                                             const double (&vec)[L][L], const double (&w)[L], int64_t o);
+template <int L>
 __device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>& D, int64_t o) {
     double vec[L][L], w[L];
     dwest_eigen<L>(D.cd, vec, w);
+    dwest_select<L>(R, D, vec, w, o);
+}
+template <int L>
+__device__ __forceinline__ void dwest_select(const ReqDev& R, const DualStats<L>& D,
+                                             const double (&vec)[L][L], const double (&w)[L], int64_t o) {
     // With eigenvalues sorted descending the reference loop sums v_i . m_diff while
     // lambda_i > 0 && lambda_i >= f lambda0 and stops at the first failure
     // (detect.cpp:255-262). The condition is monotone in lambda_i, so the summed set
@@ -838,6 +868,90 @@ __device__ __forceinline__ void select_box(const double (&S)[NBOX][Dim<L>::NC], 
         }
 }
 
+// The standard trio (one LRX on the outer window, one DWRX and one DWEST on (outer,
+// inner)): the LRX and DWRX Cholesky chains (fp64 pipe) and the DWEST fp32 Jacobi stage
+// (FMA pipe, sweeps unrolled) are independent and sit in one basic block, so the
+// scheduler interleaves them and both pipes work at once. Same per-value arithmetic as
+// lrx_solve / dwrx_solve / dwest_solve, so results are bit-identical to those paths.
+template <int L, bool ZC>
+__device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* s_req,
+                                           const double (&S0)[Dim<L>::NC], const double (&S1)[Dim<L>::NC],
+                                           int cnt0, int cnt1, int nzc, const double (&yc)[L], int64_t r,
+                                           int64_t col, int64_t o, int64_t lin) {
+    constexpr int NC = Dim<L>::NC;
+    const int qL = P.trio_q[0], qR = P.trio_q[1], qE = P.trio_q[2];
+    const ReqDev& RL = s_req[qL];
+    const ReqDev& RR = s_req[qR];
+    const ReqDev& RE = s_req[qE];
+    double bg[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) bg[c] = S0[c];
+    add_moments<L>(bg, yc, -1.0);
+    const bool bg_zero = ZC && cnt0 - nzc == 0;
+    double muL[L], cm[L][L], dv[L];
+    mean_cov<L>(bg, RL.n_a, muL, cm, false);
+    double dmaxL = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        dv[i] = yc[i] - muL[i];
+        dmaxL = fmax(dmaxL, fabs(dv[i]));
+    }
+    DualStats<L> D;
+    dual_stats<L>(S1, S0, P.n_in, P.n_ann, ZC && cnt1 == 0, ZC && cnt0 - cnt1 == 0, D);
+    double a[L][L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = i; j < L; ++j) a[i][j] = D.c_out[i][j];
+    // the three independent chains
+    double scoreL = 0.0, deltaL = 0.0, scoreR = 0.0, deltaR = 0.0;
+    int codeL = chol_quad<L>(cm, dv, RL.ridge, scoreL, deltaL);
+    int codeR = chol_quad<L>(a, D.md, RR.ridge, scoreR, deltaR);
+    float v32[L][L];
+    dwest_f32_stage<L, true>(D.cd, v32);
+    // LRX epilogue (lrx_solve)
+    if (bg_zero) {
+        if (nzc) report(P, qL, r, col, HSAD_E_SINGULAR_AFTER_RIDGE);
+        store_score(RL, o, 0.0);
+    } else {
+        double score = 0.0;
+        if (dmaxL > 0.0) {
+            if (lin == P.diag_lin && P.req_base + qL == P.diag_req) *P.diag_out = deltaL;
+            score = scoreL;
+            if (codeL == kIllConditioned) {
+                if constexpr (ZC) codeL = repair_pixel<L>(P, RL, r, col, score);
+                else s_zero_seen = 1, codeL = 0;
+            }
+            if (codeL) {
+                report(P, qL, r, col, codeL);
+                score = 0.0;
+            }
+        }
+        store_score(RL, o, fmax(score, 0.0));
+    }
+    // DWRX epilogue (dwrx_solve)
+    {
+        double score = 0.0;
+        if (D.mmax > 0.0) {
+            if (lin == P.diag_lin && P.req_base + qR == P.diag_req) *P.diag_out = deltaR;
+            score = scoreR;
+            if (codeR == kIllConditioned) {
+                if constexpr (ZC) codeR = repair_pixel<L>(P, RR, r, col, score);
+                else s_zero_seen = 1, codeR = 0;
+            }
+            if (codeR) {
+                report(P, qR, r, col, codeR);
+                score = 0.0;
+            }
+        }
+        store_score(RR, o, fabs(score));
+    }
+    // DWEST (dwest_solve)
+    double vec[L][L], w[L];
+    dwest_f64_stage<L>(D.cd, v32, vec, w);
+    dwest_select<L>(RE, D, vec, w, o);
+}
+
 // Per-pixel solves of every request from the box sums S (detect.cpp:168-271).
 // Requests come from shared memory (s_req). In the standard layout — box 0 the
 // shared outer/LRX window, box 1 the inner box, LRX excluding only the centre —
@@ -853,6 +967,12 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
     const int64_t o = (r - P.row_begin) * P.samples + col;
     const int64_t lin = r * P.samples + col;
     if (STD || P.std_layout) {
+        if constexpr (NBOX == 2) {
+            if (P.trio) {
+                solve_trio<L, ZC>(P, s_req, S[0], S[1], cnt[0], cnt[1], nzc, yc, r, col, o, lin);
+                return;
+            }
+        }
         for (int q = 0; q < P.nreq; ++q) {
             const ReqDev& R = s_req[q];
             if (R.algo != HSAD_LRX) continue;
@@ -1423,6 +1543,16 @@ hsad_status plan_requests(const hsad_detect_request* reqs, int n, Plan& plan) {
             P.has_dual = 1;
             P.n_in = d.n_a;
             P.n_ann = d.n_b;
+        }
+    }
+    // the standard trio: one LRX, one DWRX, one DWEST (solve_trio)
+    P.trio = 0;
+    if (P.std_layout && P.nbox == 2 && n == 3) {
+        int seen[3] = {-1, -1, -1};
+        for (int q = 0; q < n; ++q) seen[P.req[q].algo] = q;
+        if (seen[0] >= 0 && seen[1] >= 0 && seen[2] >= 0 && !getenv("HSAD_NO_TRIO")) {
+            P.trio = 1;
+            for (int a = 0; a < 3; ++a) P.trio_q[a] = seen[a];
         }
     }
     P.rmax = 0;
