@@ -94,6 +94,9 @@ struct DetectParams {
     int nreq;
     ReqDev req[kMaxRequests];
     int std_layout;  // box 0 = LRX/outer window for every request, box 1 = inner box
+    const float* raw;      // FUSE: the fp32 full-band cube (same buffer rows as `cube`) ...
+    int raw_bands;         // ... its band count,
+    const double* wmap;    // ... and the composed wavelet map (4 x raw_bands)
     int trio;        // std layout with exactly one LRX, one DWRX and one DWEST request ...
     int trio_q[3];   // ... at these request positions (solve_trio interleaves their solves)
     int staged;      // STD kernel: the update rows arrive in shared memory by TMA bulk copies
@@ -113,6 +116,12 @@ struct Dim {
     static constexpr int NC2 = (NC + 1) / 2;        // channel pairs
     static constexpr int S2 = NC2 | 1;              // odd double2 stride: conflict-free LDS.128
 };
+
+// TMA row stage of the STD kernel: entering + leaving row of every box, strip width
+__host__ __device__ inline size_t stage_bytes(int nbox, int64_t ncol, int bands) {
+    return static_cast<size_t>(2 * nbox) * ncol * bands * sizeof(double);
+}
+constexpr int kFuseMapBytes = 256 * 4 * 8;  // fused DWT: the wavelet map for <= 256 bands
 
 // nonzero-count table: NBOX x ncol ints, in double2 (16-byte) units
 __host__ __device__ inline int nz_pairs(int nbox, int ncol) { return (nbox * ncol * 4 + 15) / 16; }
@@ -141,7 +150,9 @@ __device__ __forceinline__ int mirror32(int i, int n) {
 
 // y = spectrum at (global row vrow, this thread's data column) as fp64;
 // F64: the cube is known to be fp64 (no fp32 branch in the code)
-template <int L, bool F64 = false>
+// CG: the cube is written by this kernel (fused DWT): coherent L2 loads, not the
+// read-only path
+template <int L, bool F64 = false, bool CG = false>
 __device__ __forceinline__ void load_row(const DetectParams& P, const char* colbase,
                                          int64_t row_bytes, int vrow, double (&y)[L]) {
     const int drow = mirror32(vrow, static_cast<int>(P.lines)) - static_cast<int>(P.buf_row0);
@@ -151,7 +162,8 @@ __device__ __forceinline__ void load_row(const DetectParams& P, const char* colb
         if constexpr (L % 2 == 0) {
 #pragma unroll
             for (int i = 0; i < L; i += 2) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(d + i));
+                const double2 v = CG ? __ldcg(reinterpret_cast<const double2*>(d + i))
+                                     : __ldg(reinterpret_cast<const double2*>(d + i));
                 y[i] = v.x;
                 y[i + 1] = v.y;
             }
@@ -1049,7 +1061,58 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
 //   3. barrier before the next row's update.
 // Smem column stride: S2 double2 per column plus one pad pair after every K
 // columns, so the per-thread segments (stride K columns) hit distinct banks.
-template <int L, int NBOX, int K, bool STD, bool ZC>
+// Fused DWT: one reduced row of the strip (global row `grow`, already
+// inside the image) from the fp32 full-band rows, written to the reduced buffer. The
+// arithmetic is K1's lane-split kernel's exactly (reduce.cu: lane l accumulates bands
+// l + 32 s in s order for each of 8 pixels, then the same 31-shuffle butterfly), so the
+// reduced values are bit-identical to hsad_reduce's. Warps take groups of 8 strip columns.
+__device__ __forceinline__ void fused_dwt_row(const DetectParams& P, const double* wsm, int64_t grow,
+                                              int64_t c0, int ncol) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int RB = P.raw_bands, bpl = (RB + 31) >> 5;
+    const int64_t drow = grow - P.buf_row0;
+    double* red = const_cast<double*>(static_cast<const double*>(P.cube));
+    for (int g = warp; g * 8 < ncol; g += nwarps) {
+        double v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = min(g * 8 + j, ncol - 1);  // a repeated column past the strip: dropped below
+            const int dcol = mirror32(static_cast<int>(c0 - P.rmax + c), static_cast<int>(P.samples));
+            const float* px = P.raw + (drow * P.samples + dcol) * RB;
+#pragma unroll 8
+            for (int s2 = 0; s2 < 8; ++s2) {
+                if (s2 >= bpl) break;
+                const int b = lane + 32 * s2;
+                const double x = b < RB ? static_cast<double>(__ldg(px + b)) : 0.0;
+                const double* w = wsm + (s2 * 32 + lane) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[j * 4 + k] = fma(w[k], x, v[j * 4 + k]);
+            }
+        }
+        // butterfly reduce-scatter (reduce.cu): lane l ends with output l = (pixel l/4, band l%4)
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+                const double send = upper ? v[i] : v[i + o];
+                const double keep = upper ? v[i + o] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        const int c = g * 8 + (lane >> 2);
+        if (c < ncol) {
+            const int dcol = mirror32(static_cast<int>(c0 - P.rmax + c), static_cast<int>(P.samples));
+            red[(drow * P.samples + dcol) * 4 + (lane & 3)] = v[0];
+        }
+    }
+    // the rows are read back by this CTA's TMA bulk copies (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int L, int NBOX, int K, bool STD, bool ZC, bool FUSE = false>
 // 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
 // fp64 operations, and extra warps hide their latency better than the registers
 // a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
@@ -1089,11 +1152,31 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
     if (ra >= rb) return;
     const int64_t row_bytes = P.samples * L * P.elem_bytes;
 
+    const int64_t st_lo = c0 - P.rmax > 0 ? c0 - P.rmax : 0;
+    const int64_t st_hi = c0 + P.tw + P.rmax < P.samples ? c0 + P.tw + P.rmax : P.samples;
+    // per strip column and box: nonzero spectra in the column's vertical window (kept
+    // like the window sums: + entering row, - leaving row)
+    int* s_nz = reinterpret_cast<int*>(s_v2 + NBOX * box_stride);  // [NBOX][ncol]
+    double* stage = reinterpret_cast<double*>(s_v2 + NBOX * box_stride + nz_pairs(NBOX, ncol));
+    const double* wsm = stage + stage_bytes(NBOX, ncol, L) / sizeof(double);  // FUSE: wavelet map
+    if constexpr (FUSE) {
+        // the composed map, band-major: wsm[b][k] (lane-contiguous for the DWT)
+        double* w = const_cast<double*>(wsm);
+        for (int e = t; e < 256 * 4; e += NT) {
+            const int b = e >> 2, k = e & 3;
+            w[e] = b < P.raw_bands ? P.wmap[k * P.raw_bands + b] : 0.0;
+        }
+        __syncthreads();
+        // warm-up: the reduced rows the first window and the first staged update read
+        for (int64_t d = -P.radius[0]; d <= P.radius[0] + 1; ++d)
+            fused_dwt_row(P, wsm, mirror32(static_cast<int>(ra + d), static_cast<int>(P.lines)), c0, ncol);
+        __syncthreads();
+    }
     // tile-anchored shift: the spectrum at (ra, c0)
     double shift[L];
     {
         double y[L];
-        load_row<L, STD>(P, static_cast<const char*>(P.cube) + c0 * L * P.elem_bytes, row_bytes,
+        load_row<L, STD, FUSE>(P, static_cast<const char*>(P.cube) + c0 * L * P.elem_bytes, row_bytes,
                     static_cast<int>(ra), y);
 #pragma unroll
         for (int i = 0; i < L; ++i) shift[i] = y[i];
@@ -1104,7 +1187,7 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
         return static_cast<const char*>(P.cube) + static_cast<int64_t>(dcol) * L * P.elem_bytes;
     };
     auto shifted = [&](const char* cb, int64_t vrow, double (&y)[L]) -> int {
-        load_row<L, STD>(P, cb, row_bytes, static_cast<int>(vrow), y);
+        load_row<L, STD, FUSE>(P, cb, row_bytes, static_cast<int>(vrow), y);
         const int nz = nonzero<L>(y);
 #pragma unroll
         for (int i = 0; i < L; ++i) y[i] -= shift[i];
@@ -1116,13 +1199,6 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
     // row: the strip's clipped column range is contiguous in BIP) into a shared
     // stage while the CTA still solves row rr - 1, so the update reads shared
     // memory instead of waiting on L2/HBM. stage[(2k + dir) * ncol + col][L].
-    const int64_t st_lo = c0 - P.rmax > 0 ? c0 - P.rmax : 0;
-    const int64_t st_hi = c0 + P.tw + P.rmax < P.samples ? c0 + P.tw + P.rmax : P.samples;
-    // per strip column and box: count of nonzero spectra in the vertical window
-    // per strip column and box: nonzero spectra in the column's vertical window (kept
-    // like the window sums: + entering row, - leaving row)
-    int* s_nz = reinterpret_cast<int*>(s_v2 + NBOX * box_stride);  // [NBOX][ncol]
-    double* stage = reinterpret_cast<double*>(s_v2 + NBOX * box_stride + nz_pairs(NBOX, ncol));
     auto issue_rows = [&](int64_t rr) {  // thread 0 only
         const uint32_t seg = static_cast<uint32_t>((st_hi - st_lo) * L * sizeof(double));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1350,6 +1426,11 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
                 PT_MARK(3);  // solves
             }
         }
+        if constexpr (FUSE) {  // the entering row of the TMA copies issued at step r + 1
+            if (r + 2 < rb)
+                fused_dwt_row(P, wsm, mirror32(static_cast<int>(r + 2 + P.radius[0]), static_cast<int>(P.lines)),
+                              c0, ncol);
+        }
         __syncthreads();
         PT_MARK(4);  // barrier B
     }
@@ -1360,18 +1441,14 @@ __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) det
     PT_FLUSH();
 }
 
-// TMA row stage of the STD kernel: entering + leaving row of every box, strip width
-size_t stage_bytes(int nbox, int64_t ncol, int bands) {
-    return static_cast<size_t>(2 * nbox) * ncol * bands * sizeof(double);
-}
 
 template <int L, int NB>
 cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
     const int ncol = P.tw + 2 * P.rmax;
-    auto go = [&](auto kern, int K, bool staged, bool two_pass) -> cudaError_t {
+    auto go = [&](auto kern, int K, bool staged, bool two_pass, bool fused = false) -> cudaError_t {
         const size_t smem = (static_cast<size_t>(NB) * (ncol * Dim<L>::S2 + (K > 1 ? ncol / K + 1 : 0)) +
                              nz_pairs(NB, ncol)) * sizeof(double2) +
-                            (staged ? stage_bytes(NB, ncol, L) : 0);
+                            (staged ? stage_bytes(NB, ncol, L) : 0) + (fused ? kFuseMapBytes : 0);
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
@@ -1395,6 +1472,12 @@ cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaS
                     cudaError_t e = go(fast, K, true, true);
                     return e != cudaSuccess ? e : go(counting, K, true, true);
                 };
+                if constexpr (NB == 2) {
+                    if (P.raw && kcols == 1) {  // fused DWT fast pass (the counting pass reads the rows it wrote)
+                        cudaError_t e = go(detect_kernel<L, NB, 1, true, false, true>, 1, true, true, true);
+                        return e != cudaSuccess ? e : go(detect_kernel<L, NB, 1, true, true>, 1, true, true);
+                    }
+                }
                 if (kcols == 4) return both(detect_kernel<L, NB, 4, true, false>, detect_kernel<L, NB, 4, true, true>, 4);
                 if (kcols == 2) return both(detect_kernel<L, NB, 2, true, false>, detect_kernel<L, NB, 2, true, true>, 2);
                 if (kcols == 1) return both(detect_kernel<L, NB, 1, true, false>, detect_kernel<L, NB, 1, true, true>, 1);
@@ -1589,17 +1672,37 @@ int64_t row_quantum(int64_t lines, int64_t samples) {
 
 namespace {
 
+// hsad_reduce_detect's reduction, folded into the first detector launch when it can be
+// (fused_dwt_row): the fp32 cube, its bands and the composed map; `done` reports whether
+// the reduced buffer was written by the fused launch or by hsad_reduce before it.
+struct FuseArgs {
+    const float* raw;
+    int bands, order, target;
+    const double* map;
+    bool fused = false;    // the first launch computed the reduction
+    bool reduced = false;  // hsad_reduce ran before it
+};
+
 // One fused launch: <= kMaxRequests requests over <= kMaxBoxes window sizes.
 hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
                               int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
                               int64_t row_begin, int64_t row_end,
                               const hsad_detect_request* requests, int32_t n_requests,
                               int req_base, uint64_t* d_status, hsad_pixel_error* err,
-                              cudaStream_t s) {
+                              cudaStream_t s, FuseArgs* fuse = nullptr) {
     if (err) {
         err->code = HSAD_OK;
         err->row = err->col = -1;
     }
+    // the reduction when it is not fused into this launch (every early return below)
+    auto reduce_first = [&]() -> hsad_status {
+        if (!fuse) return HSAD_OK;
+        FuseArgs* f = fuse;
+        fuse = nullptr;
+        f->reduced = true;
+        return hsad_reduce(f->raw, 4, buf_rows, samples, f->bands, f->order, f->target,
+                           const_cast<void*>(d_cube), 8, s);
+    };
     Plan plan;
     hsad_status st = plan_requests(requests, n_requests, plan);
     if (st != HSAD_OK) return st;
@@ -1610,7 +1713,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
     if (bands < 1) return set_error(HSAD_E_INVALID_VALUE, "cube has no bands");
     if (lines < 0 || samples < 0 || row_begin < 0 || row_end > lines || row_begin > row_end)
         return set_error(HSAD_E_INVALID_VALUE, "row range outside the image");
-    if (row_begin == row_end || samples == 0) return HSAD_OK;
+    if (row_begin == row_end || samples == 0) return reduce_first();
     // rows the windows touch must be resident in the buffer
     int64_t need0 = 0, need_rows = 0;
     st = hsad_strip_rows(lines, row_begin, row_end, requests, n_requests, &need0, &need_rows);
@@ -1632,6 +1735,8 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                 err->col = 0;
             }
             // detect.cpp:127-130 rethrows with the inner "<Name>: " kept
+            const hsad_status rs = reduce_first();
+            if (rs != HSAD_OK) return rs;
             return set_error(HSAD_E_TOO_FEW_SAMPLES,
                              "TooFewSamples: covariance needs at least 2 samples, got 1 at pixel (" +
                                  std::to_string(row_begin) + ", 0)");
@@ -1679,6 +1784,26 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                    smem_cap &&
                !getenv("HSAD_NO_STAGE");
     P.req_base = req_base;
+    P.raw = nullptr;
+    P.raw_bands = 0;
+    P.wmap = nullptr;
+    if (fuse) {
+        const int64_t ncol = P.tw + 2 * P.rmax;
+        const bool fits = smem_for(kc) + static_cast<int64_t>(stage_bytes(P.nbox, ncol, bands)) +
+                              kFuseMapBytes <= smem_cap;
+        // the fused launch writes exactly the rows its windows read: it must be the whole buffer
+        if (P.staged && kc == 1 && P.nbox == 2 && bands == 4 && fuse->bands <= 256 && fits &&
+            need0 == buf_row0 && need_rows == buf_rows && !fullband && !getenv("HSAD_NO_FUSE")) {
+            P.raw = fuse->raw;
+            P.raw_bands = fuse->bands;
+            P.wmap = fuse->map;
+            fuse->fused = true;
+            fuse = nullptr;
+        } else {
+            st = reduce_first();
+            if (st != HSAD_OK) return st;
+        }
+    }
     P.diag_lin = -1;
     P.diag_req = -1;
     P.diag_out = nullptr;
@@ -1765,6 +1890,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             double delta = 0.0;
             double* d_diag = reinterpret_cast<double*>(status) + 1;
             DetectParams D = P;
+            D.raw = nullptr;  // the reduced rows exist now
             D.row_begin = row;
             D.row_end = row + 1;
             D.diag_lin = lin;
@@ -1827,11 +1953,13 @@ int request_radii(const hsad_detect_request& r, int (&out)[2]) {
 // distinct window sizes; each group is one fused launch. The grouping (and so the
 // launch shape) depends only on the request list, so results are deterministic. Synchronous calls report the first group (in request order) with a
 // failing pixel, i.e. the first of the equivalent sequential hsad::detect calls.
-hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
+namespace {
+hsad_status detect_multi_fuse(const void* d_cube, int32_t elem_bytes, int64_t lines,
                               int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
                               int64_t row_begin, int64_t row_end,
                               const hsad_detect_request* requests, int32_t n_requests,
-                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s) {
+                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s,
+                              FuseArgs* fuse) {
     if (n_requests < 1 || n_requests > kMaxCallRequests || !requests)
         return set_error(HSAD_E_INVALID_VALUE, "between 1 and " + std::to_string(kMaxCallRequests) +
                                                    " requests per call");
@@ -1863,16 +1991,30 @@ hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t li
         }
         hsad_status st = detect_group_impl(d_cube, elem_bytes, lines, samples, bands, buf_row0,
                                            buf_rows, row_begin, row_end, requests + g0, g1 - g0, g0,
-                                           d_status, err, s);
+                                           d_status, err, s, g0 == 0 ? fuse : nullptr);
         if (st != HSAD_OK) return st;
         g0 = g1;
     }
     return HSAD_OK;
 }
+}  // namespace
+
+hsad_status detect_multi_impl(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                              int64_t samples, int32_t bands, int64_t buf_row0, int64_t buf_rows,
+                              int64_t row_begin, int64_t row_end,
+                              const hsad_detect_request* requests, int32_t n_requests,
+                              uint64_t* d_status, hsad_pixel_error* err, cudaStream_t s) {
+    return detect_multi_fuse(d_cube, elem_bytes, lines, samples, bands, buf_row0, buf_rows, row_begin,
+                             row_end, requests, n_requests, d_status, err, s, nullptr);
+}
 
 }  // namespace hsad_b200
 
 using namespace hsad_b200;
+
+namespace {
+thread_local int32_t g_last_fused = 0;
+}
 
 #ifdef HSAD_PHASE_TIMERS
 extern "C" void hsad_phase_cycles(unsigned long long* out, int reset) {
@@ -1887,6 +2029,8 @@ extern "C" void hsad_phase_cycles(unsigned long long* out, int reset) {
 extern "C" {
 
 int64_t hsad_row_quantum(int64_t lines, int64_t samples) { return row_quantum(lines, samples); }
+
+int32_t hsad_last_reduce_detect_fused(void) { return g_last_fused; }
 
 hsad_status hsad_strip_rows(int64_t lines, int64_t row_begin, int64_t row_end,
                             const hsad_detect_request* requests, int32_t n_requests,
@@ -1941,12 +2085,23 @@ hsad_status hsad_reduce_detect(const float* d_cube, int64_t lines, int64_t sampl
     if (buf_row0 < 0 || buf_rows < 0 || buf_row0 + buf_rows > lines)
         return set_error(HSAD_E_INVALID_VALUE, "buffer rows outside the image");
     // reduce_cube errors first (the CLI runs `hsad reduce` before `hsad detect`)
-    hsad_status st = hsad_reduce(d_cube, 4, buf_rows, samples, bands, order, target_bands,
-                                 d_reduced, 8, stream);
+    const double* d_map = nullptr;
+    hsad_status st = device_wavelet_map(bands, order, target_bands, &d_map);
     if (st != HSAD_OK) return st;
-    return detect_multi_impl(d_reduced, 8, lines, samples, target_bands, buf_row0, buf_rows,
-                             row_begin, row_end, requests, n_requests, d_status, err,
-                             static_cast<cudaStream_t>(stream));
+    if (!d_cube || !d_reduced) return set_error(HSAD_E_INVALID_VALUE, "null buffer");
+    // the reduction runs inside the first detector launch when it can (fused_dwt_row),
+    // else hsad_reduce runs first; either way the reduced rows are bit-identical
+    FuseArgs fa{d_cube, bands, order, target_bands, d_map};
+    st = detect_multi_fuse(d_reduced, 8, lines, samples, target_bands, buf_row0, buf_rows, row_begin,
+                           row_end, requests, n_requests, d_status, err, static_cast<cudaStream_t>(stream),
+                           &fa);
+    if (!fa.fused && !fa.reduced) {  // a request error before any launch: the reduction still runs
+        const hsad_status rs = hsad_reduce(d_cube, 4, buf_rows, samples, bands, order, target_bands,
+                                           d_reduced, 8, stream);
+        if (st == HSAD_OK) st = rs;
+    }
+    g_last_fused = fa.fused ? 1 : 0;
+    return st;
 }
 
 hsad_status hsad_detect(const void* d_cube, int32_t elem_bytes, int64_t lines, int64_t samples,
