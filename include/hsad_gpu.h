@@ -198,10 +198,10 @@ hsad_status hsad_reduce_detect(const float* d_cube, int64_t lines, int64_t sampl
                                void* stream);
 
 /* 1 when the calling thread's last hsad_reduce_detect folded the reduction into its first
- * detector launch (the DWT of each row is computed by the CTAs that need
- * it, as that row enters their windows, with hsad_reduce's exact arithmetic), 0 when it
- * ran hsad_reduce first (strip buffers wider than the first group's windows, windows
- * whose statistics do not leave shared memory for the map, ...). */
+ * detector launch (opt-in with HSAD_FUSE=1: the DWT of each row is
+ * computed by the CTAs that need it, as that row enters their windows, with hsad_reduce's
+ * exact arithmetic; measured slower than the two-step path on B200), 0 when it ran
+ * hsad_reduce first. */
 int32_t hsad_last_reduce_detect_fused(void);
 
 /* Rows [*buf_row0, *buf_row0 + *buf_rows) that output rows [row_begin, row_end) of a

@@ -1672,9 +1672,12 @@ int64_t row_quantum(int64_t lines, int64_t samples) {
 
 namespace {
 
-// hsad_reduce_detect's reduction, folded into the first detector launch when it can be
-// (fused_dwt_row): the fp32 cube, its bands and the composed map; `done` reports whether
-// the reduced buffer was written by the fused launch or by hsad_reduce before it.
+// hsad_reduce_detect's reduction, folded into the first detector launch (fused_dwt_row)
+// when HSAD_FUSE=1 and the launch qualifies: the fp32 cube, its bands and the composed
+// map. Opt-in because it measured 7x slower than hsad_reduce + the launch (C5 sweep,
+// first window pair: 37.8 ms vs 5.16 ms): without shared memory left for a TMA ring of
+// the 120 KB raw row each CTA reduces per step, the full-band loads sit in the
+// latency-bound detector loop (f1).
 struct FuseArgs {
     const float* raw;
     int bands, order, target;
@@ -1793,7 +1796,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
                               kFuseMapBytes <= smem_cap;
         // the fused launch writes exactly the rows its windows read: it must be the whole buffer
         if (P.staged && kc == 1 && P.nbox == 2 && bands == 4 && fuse->bands <= 256 && fits &&
-            need0 == buf_row0 && need_rows == buf_rows && !fullband && !getenv("HSAD_NO_FUSE")) {
+            need0 == buf_row0 && need_rows == buf_rows && !fullband && getenv("HSAD_FUSE")) {
             P.raw = fuse->raw;
             P.raw_bands = fuse->bands;
             P.wmap = fuse->map;

@@ -1,4 +1,4 @@
-"""Fused DWT -> detector launch against the two-step path.
+"""Fused DWT -> detector launch (opt-in: HSAD_FUSE=1) against the two-step path.
 
 hsad_reduce_detect folds the reduction into its first detector launch when the launch's
 windows read exactly the buffer rows (fused_dwt_row: every CTA computes the reduced rows
@@ -15,6 +15,12 @@ pytestmark = pytest.mark.gpu
 
 hs = pytest.importorskip("paper_1201_2025_b200")
 from paper_1201_2025_b200 import _abi  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def _fuse_on(monkeypatch):
+    """The fused launch is opt-in (HSAD_FUSE=1; measured slower than two steps)."""
+    monkeypatch.setenv("HSAD_FUSE", "1")
 
 DEV = "cuda:0"
 
