@@ -32,7 +32,9 @@ def label(i, name, seen):
     zero-window counting pass that follows each fast pass."""
     if "reduce" in name:
         return "reduce (K1)"
-    if name.replace(" ", "").split("(")[0].endswith(",1,1>"):
+    args = name.split("detect_kernel<", 1)[1].split(">", 1)[0].replace("(bool)", "").replace("(int)", "")
+    args = [a.strip() for a in args.split(",")]
+    if len(args) >= 5 and args[4] in ("1", "true"):  # ZC: the zero-window counting pass
         return f"detect {WINDOWS[(seen['fast'] - 1) % 4]} counting pass"
     seen["fast"] += 1
     return f"detect {WINDOWS[(seen['fast'] - 1) % 4]}"
