@@ -370,11 +370,13 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // makes the denominator vanish; that case is selected to t = 0.
 __device__ __forceinline__ float jacobi_t32(float app, float aqq, float apq) {
     const float h = aqq - app;
-    const float r2 = fmaf(4.0f * apq, apq, h * h);
-    const float den = mad(r2, rsqrtf(r2), fabsf(h));
-    float t = 2.0f * apq * rcp_approx(den);
-    t = h < 0.0f ? -t : t;
-    return den > 0.0f ? t : 0.0f;
+    const float apq2 = apq + apq;
+    const float r2 = mad(apq2, apq2, h * h);
+    // h = apq = 0: r2 * rsqrt(r2) is NaN and fmaxf keeps FLT_MIN, so t = 0 * huge = 0
+    const float den = fmaxf(mad(r2, rsqrtf(r2), fabsf(h)), FLT_MIN);
+    const float t = apq2 * rcp_approx(den);
+    // sign of h (for h = +-0 either sign zeroes a_pq)
+    return __int_as_float(__float_as_int(t) ^ (__float_as_int(h) & 0x80000000));
 }
 
 // fp64 general-path angle (fast rcp/rsqrt, ~1 ulp)
