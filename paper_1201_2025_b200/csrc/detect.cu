@@ -389,6 +389,16 @@ __device__ __forceinline__ double jacobi_t64(double app, double aqq, double apq)
     return den > 0.0 ? t : 0.0;
 }
 
+// The polish sweep's general angle (some lane of the warp still has a large angle):
+// rare after the fp32 stage, so kept out of line to spare the instruction cache.
+__device__ __noinline__ void polish_angle_general(double app, double aqq, double apq, bool small,
+                                                  double& t, double& c) {
+    const double h = aqq - app;
+    t = small ? (apq == 0.0 ? 0.0 : apq * fast_rcp(h)) : jacobi_t64(app, aqq, apq);
+    if (small) t = t * fma(-t, t, 1.0);
+    c = fast_rsqrt(fma(t, t, 1.0));
+}
+
 // Pairs of one sweep; for L = 4 in parallel order (rounds of two disjoint pairs
 // {(0,1),(2,3)}, {(0,2),(1,3)}, {(0,3),(1,2)} whose angles are independent).
 template <int L>
@@ -478,9 +488,7 @@ __device__ __forceinline__ void sweep64(double (&a)[L][L], double (&v)[L][L]) {
             t = x * fma(-x, x, 1.0);
             c = fma(-0.5 * t, t, 1.0);
         } else {
-            t = small ? (apq == 0.0 ? 0.0 : apq * fast_rcp(h)) : jacobi_t64(a[p][p], a[q][q], apq);
-            if (small) t = t * fma(-t, t, 1.0);
-            c = fast_rsqrt(fma(t, t, 1.0));
+            polish_angle_general(a[p][p], a[q][q], apq, small, t, c);
         }
         rotate_tc<L, double>(a, v, p, q, t, c);
     }
@@ -883,10 +891,10 @@ __device__ __forceinline__ void select_box(const double (&S)[NBOX][Dim<L>::NC], 
 }
 
 // The standard trio (one LRX on the outer window, one DWRX and one DWEST on (outer,
-// inner)): the LRX and DWRX Cholesky chains (fp64 pipe) and the DWEST fp32 Jacobi stage
-// (FMA pipe, sweeps unrolled) are independent and sit in one basic block, so the
-// scheduler interleaves them and both pipes work at once. Same per-value arithmetic as
-// lrx_solve / dwrx_solve / dwest_solve, so results are bit-identical to those paths.
+// inner)): the three solves without the per-request dispatch of the general path, the
+// LRX and DWRX Cholesky chains side by side so the scheduler can interleave them. Same
+// per-value arithmetic as lrx_solve / dwrx_solve / dwest_solve, so results are
+// bit-identical to those paths.
 template <int L, bool ZC>
 __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* s_req,
                                            const double (&S0)[Dim<L>::NC], const double (&S1)[Dim<L>::NC],
@@ -917,12 +925,14 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
     for (int i = 0; i < L; ++i)
 #pragma unroll
         for (int j = i; j < L; ++j) a[i][j] = D.c_out[i][j];
-    // the three independent chains
+    // the LRX and DWRX solves
     double scoreL = 0.0, deltaL = 0.0, scoreR = 0.0, deltaR = 0.0;
     int codeL = chol_quad<L>(cm, dv, RL.ridge, scoreL, deltaL);
     int codeR = chol_quad<L>(a, D.md, RR.ridge, scoreR, deltaR);
     float v32[L][L];
-    dwest_f32_stage<L, true>(D.cd, v32);
+    // the sweeps stay a loop: unrolled, the kernel outgrows the instruction cache
+    // (measured 4.6% slower on the C5 sweep)
+    dwest_f32_stage<L>(D.cd, v32);
     // LRX epilogue (lrx_solve)
     if (bg_zero) {
         if (nzc) report(P, qL, r, col, HSAD_E_SINGULAR_AFTER_RIDGE);
@@ -971,7 +981,7 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
 // shared outer/LRX window, box 1 the inner box, LRX excluding only the centre —
 // box indices are compile-time and the inner/annulus statistics are computed
 // once for DWRX and DWEST; other layouts select boxes at run time.
-template <int L, int NBOX, bool STD, bool ZC>
+template <int L, int NBOX, bool STD, bool ZC, bool TRIO = false>
 __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev* s_req,
                                             const double (&S)[NBOX][Dim<L>::NC],
                                             const int (&cnt)[NBOX], int nzc, const double (&yc)[L],
@@ -980,6 +990,10 @@ __device__ __forceinline__ void solve_pixel(const DetectParams& P, const ReqDev*
     constexpr int NC = Dim<L>::NC;
     const int64_t o = (r - P.row_begin) * P.samples + col;
     const int64_t lin = r * P.samples + col;
+    if constexpr (TRIO && NBOX == 2) {  // a kernel for the trio alone (no general paths: smaller code)
+        solve_trio<L, ZC>(P, s_req, S[0], S[1], cnt[0], cnt[1], nzc, yc, r, col, o, lin);
+        return;
+    }
     if (STD || P.std_layout) {
         if constexpr (NBOX == 2) {
             if (P.trio) {
@@ -1114,7 +1128,7 @@ __device__ __forceinline__ void fused_dwt_row(const DetectParams& P, const doubl
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int L, int NBOX, int K, bool STD, bool ZC, bool FUSE = false>
+template <int L, int NBOX, int K, bool STD, bool ZC, bool FUSE = false, bool TRIO = false>
 // 4 resident CTAs (16 warps) per SM: the per-pixel solves are chains of dependent
 // fp64 operations, and extra warps hide their latency better than the registers
 // a larger budget would save (measured: 4.35 vs 5.52 ms for LRX+DWRX+DWEST on C5).
@@ -1424,7 +1438,7 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
                     nzc = shifted(colbase_of(P.rmax + sc), r, yc);
                 }
                 PT_MARK(2);  // horizontal + centre load
-                solve_pixel<L, NBOX, STD, ZC>(P, s_req, S, cnt, nzc, yc, r, col);
+                solve_pixel<L, NBOX, STD, ZC, TRIO>(P, s_req, S, cnt, nzc, yc, r, col);
                 PT_MARK(3);  // solves
             }
         }
@@ -1447,9 +1461,9 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
     PT_FLUSH();
 }
 
-template <int L, int NBOX, int K, bool STD, bool ZC, bool FUSE = false>
+template <int L, int NBOX, int K, bool STD, bool ZC, bool FUSE = false, bool TRIO = false>
 __global__ void __launch_bounds__(HSAD_DET_NT, (L <= 5 ? HSAD_DET_MINB : 1)) detect_kernel(const DetectParams P) {
-    detect_tile<L, NBOX, K, STD, ZC, FUSE>(P, blockIdx.x, blockIdx.y, gridDim.x);
+    detect_tile<L, NBOX, K, STD, ZC, FUSE, TRIO>(P, blockIdx.x, blockIdx.y, gridDim.x);
 }
 
 // The counting pass after a fast pass recomputes only the tiles the fast pass flagged
@@ -1516,6 +1530,13 @@ cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaS
                     if (P.raw && kcols == 1) {  // fused DWT fast pass (the counting pass reads the rows it wrote)
                         cudaError_t e = go(detect_kernel<L, NB, 1, true, false, true>, 1, true, true, true);
                         return e != cudaSuccess ? e : go_flagged(detect_kernel_flagged<L, NB, 1, true>, 1);
+                    }
+                }
+                if constexpr (NB == 2) {
+                    if (P.trio) {  // the standard trio's own kernel (smaller code)
+                        if (kcols == 4) return both(detect_kernel<L, NB, 4, true, false, false, true>, detect_kernel_flagged<L, NB, 4, true>, 4);
+                        if (kcols == 2) return both(detect_kernel<L, NB, 2, true, false, false, true>, detect_kernel_flagged<L, NB, 2, true>, 2);
+                        if (kcols == 1) return both(detect_kernel<L, NB, 1, true, false, false, true>, detect_kernel_flagged<L, NB, 1, true>, 1);
                     }
                 }
                 if (kcols == 4) return both(detect_kernel<L, NB, 4, true, false>, detect_kernel_flagged<L, NB, 4, true>, 4);
