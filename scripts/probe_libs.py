@@ -1,6 +1,7 @@
 """A/B probe over library builds: C5 sweep detector times per libhsad variant.
 
     python scripts/probe_libs.py variants/base.so variants/x.so ...   (each run twice, interleaved)
+    an argument may carry environment settings: lib.so,HSAD_DWEST_SPLIT=1
 Child mode (internal): HSAD_B200_LIB=<lib> python scripts/probe_libs.py --child
 """
 import os
@@ -48,7 +49,9 @@ def child():
         # checksum of the maps so variants can be compared for bit-identity
         sums.append(sum(float(o[0].double().sum()) for o in outs))
         sums.append(float(outs[2][1].double().sum()))
-    print(f"{Path(os.environ['HSAD_B200_LIB']).name:28s} " + "  ".join(line) + f"  sum {tot:.3f}",
+        # bit-level checksum (any differing bit changes it)
+        sums.append(float(sum(int(o[0].contiguous().view(torch.int64).sum()) & 0xFFFFFFFFFFFF for o in outs)))
+    print(f"{os.environ.get('PROBE_LABEL', Path(os.environ['HSAD_B200_LIB']).name):28s} " + "  ".join(line) + f"  sum {tot:.3f}",
           flush=True)
     print(f"{'':28s} checksums " + " ".join(f"{x:.15e}" for x in sums), flush=True)
 
@@ -58,6 +61,8 @@ if __name__ == "__main__":
         child()
     else:
         for rep in range(2):
-            for lib in sys.argv[1:]:
-                env = dict(os.environ, HSAD_B200_LIB=str(Path(lib).resolve()))
+            for arg in sys.argv[1:]:
+                lib, *kv = arg.split(",")
+                env = dict(os.environ, HSAD_B200_LIB=str(Path(lib).resolve()), PROBE_LABEL=arg[-28:])
+                env.update(x.split("=", 1) for x in kv)
                 subprocess.run([sys.executable, __file__, "--child"], env=env, check=False)
