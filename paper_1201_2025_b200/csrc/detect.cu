@@ -240,6 +240,11 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
     return y * fma(-h * y, y, 1.5);
 }
 
+// max / min by compare-and-select (3 instructions; fmax / fmin cost ~8 with their NaN
+// rules). For operands that are never NaN.
+__device__ __forceinline__ double max_sel(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double min_sel(double a, double b) { return a < b ? a : b; }
+
 // mean and covariance (divisor N) from box sums: C = S2/N - mu mu^T
 // (== stats.cpp:13-29 in exact arithmetic on the shifted values). Symmetric
 // matrices are stored as their upper triangle only (c[i][j], i <= j).
@@ -277,18 +282,17 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
     delta = (L & (L - 1)) == 0 ? __dmul_rn(__dmul_rn(ridge, tr), 1.0 / L) : __ddiv_rn(__dmul_rn(ridge, tr), L);
 #pragma unroll
     for (int i = 0; i < L; ++i) a[i][i] += delta;
-    double dmax = 0.0, dmin = DBL_MAX;
     bool ok = true;
-    double z[L];
+    double z[L], piv[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) {
         double p = a[j][j];
 #pragma unroll
         for (int k = 0; k < j; ++k) p = fma(-a[k][j], a[k][j], p);
         ok = ok && (p > 0.0);
-        dmax = fmax(dmax, fabs(p));
-        dmin = fmin(dmin, p);
-        const double rinv = fast_rsqrt(fmax(p, DBL_MIN));
+        piv[j] = p;
+        // a non-positive pivot makes rinv inf / NaN; the pixel is rejected below
+        const double rinv = fast_rsqrt(p);
 #pragma unroll
         for (int i = j + 1; i < L; ++i) {
             double v = a[j][i];
@@ -301,7 +305,14 @@ __device__ __forceinline__ int chol_quad(double (&a)[L][L], const double (&d)[L]
         for (int k = 0; k < j; ++k) zj = fma(-a[k][j], z[k], zj);
         z[j] = zj * rinv;
     }
-    if (!ok || !(dmax > 0.0) || dmin <= dmax * 1e-14) return HSAD_E_SINGULAR_AFTER_RIDGE;
+    if (!ok) return HSAD_E_SINGULAR_AFTER_RIDGE;
+    double dmax = piv[0], dmin = piv[0];  // all pivots positive here
+#pragma unroll
+    for (int j = 1; j < L; ++j) {
+        dmax = max_sel(dmax, piv[j]);
+        dmin = min_sel(dmin, piv[j]);
+    }
+    if (dmin <= dmax * 1e-14) return HSAD_E_SINGULAR_AFTER_RIDGE;
     double s = 0.0;
 #pragma unroll
     for (int j = 0; j < L; ++j) s = fma(z[j], z[j], s);
@@ -743,14 +754,14 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const Re
     }
     double mu[L], cm[L][L], dv[L];
     mean_cov<L>(bg, n_bg, mu, cm, false);
-    double dmax = 0.0;
+    bool dnz = false;  // max |d_i| > 0 (detect.cpp:175)
 #pragma unroll
     for (int i = 0; i < L; ++i) {
         dv[i] = yc[i] - mu[i];
-        dmax = fmax(dmax, fabs(dv[i]));
+        dnz = dnz | (fabs(dv[i]) > 0.0);
     }
     double score = 0.0;
-    if (dmax > 0.0) {
+    if (dnz) {
         double delta = 0.0;
         int code = chol_quad<L>(cm, dv, R.ridge, score, delta);
         if (code == kIllConditioned) {
@@ -769,7 +780,8 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const Re
 // inner-box / annulus statistics shared by DWRX and DWEST (detect.cpp:204-213, 244-253)
 template <int L>
 struct DualStats {
-    double c_out[L][L], cd[L][L], md[L], mmax;  // upper triangles; cd = C_in - C_ann
+    double c_out[L][L], cd[L][L], md[L];  // upper triangles; cd = C_in - C_ann
+    bool mnz;                             // max |m_diff| > 0 (detect.cpp:211)
 };
 template <int L>
 __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
@@ -786,12 +798,12 @@ __device__ __forceinline__ void dual_stats(const double (&s_in)[Dim<L>::NC],
     for (int i = 0; i < L; ++i)
 #pragma unroll
         for (int j = i; j < L; ++j) D.cd[i][j] -= D.c_out[i][j];
-    D.mmax = 0.0;
+    D.mnz = false;
     const bool both_zero = in_zero && ann_zero;  // m_diff = 0 - 0 exactly
 #pragma unroll
     for (int i = 0; i < L; ++i) {
         D.md[i] = both_zero ? 0.0 : mu_in[i] - mu_out[i];
-        D.mmax = fmax(D.mmax, fabs(D.md[i]));
+        D.mnz = D.mnz | (fabs(D.md[i]) > 0.0);
     }
 }
 
@@ -801,7 +813,7 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const R
                                            const DualStats<L>& D, int64_t r, int64_t col, int64_t o,
                                            int64_t lin) {
     double score = 0.0;
-    if (D.mmax > 0.0) {
+    if (D.mnz) {
         double a[L][L];
 #pragma unroll
         for (int i = 0; i < L; ++i)
@@ -822,41 +834,32 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const R
     store_score(R, o, fabs(score));
 }
 
-// DWEST (detect.cpp:242-271)
+// DWEST (detect.cpp:242-271): selection and projection from a full eigendecomposition.
+// With eigenvalues sorted descending the reference loop sums v_i . m_diff while
+// lambda_i > 0 && lambda_i >= f lambda0 and stops at the first failure
+// (detect.cpp:255-262). The condition is monotone in lambda_i, so the summed set
+// is exactly {i : lambda_i > 0, lambda_i >= f lambda0}: no sort needed. Sign rule
+// (stats.cpp:83-85): v_i is flipped so its first largest-|.| component is positive.
 template <int L>
-__device__ __forceinline__ void dwest_select(const ReqDev& R, const DualStats<L>& D,
-                                             const double (&vec)[L][L], const double (&w)[L], int64_t o);
-template <int L>
-__device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>& D, int64_t o) {
-    double vec[L][L], w[L];
-    dwest_eigen<L>(D.cd, vec, w);
-    dwest_select<L>(R, D, vec, w, o);
-}
-template <int L>
-__device__ __forceinline__ void dwest_select(const ReqDev& R, const DualStats<L>& D,
-                                             const double (&vec)[L][L], const double (&w)[L], int64_t o) {
-    // With eigenvalues sorted descending the reference loop sums v_i . m_diff while
-    // lambda_i > 0 && lambda_i >= f lambda0 and stops at the first failure
-    // (detect.cpp:255-262). The condition is monotone in lambda_i, so the summed set
-    // is exactly {i : lambda_i > 0, lambda_i >= f lambda0}: no sort needed. Sign rule
-    // (stats.cpp:83-85): v_i is flipped so its first largest-|.| component is positive.
+__device__ __forceinline__ void dwest_select(double frac, const double (&md)[L], const double (&vec)[L][L],
+                                             const double (&w)[L], double& score, int& count) {
     double lmax = w[0];
 #pragma unroll
     for (int i = 1; i < L; ++i) lmax = fmax(lmax, w[i]);
-    double score = 0.0;
-    int count = 0;
+    score = 0.0;
+    count = 0;
     if (lmax > 0.0) {
-        const double cut = R.frac * lmax;
+        const double cut = frac * lmax;
         double proj = 0.0;
 #pragma unroll
         for (int i = 0; i < L; ++i) {
-            double best = fabs(vec[0][i]), lead = vec[0][i], dot = vec[0][i] * D.md[0];
+            double best = fabs(vec[0][i]), lead = vec[0][i], dot = vec[0][i] * md[0];
 #pragma unroll
             for (int k = 1; k < L; ++k) {
                 const double av = fabs(vec[k][i]);
                 lead = av > best ? vec[k][i] : lead;
                 best = fmax(best, av);
-                dot = fma(vec[k][i], D.md[k], dot);
+                dot = fma(vec[k][i], md[k], dot);
             }
             const bool take = w[i] > 0.0 && !(w[i] < cut);
             proj += take ? (lead < 0.0 ? -dot : dot) : 0.0;
@@ -864,6 +867,270 @@ __device__ __forceinline__ void dwest_select(const ReqDev& R, const DualStats<L>
         }
         score = fabs(proj);
     }
+}
+
+// The general eigensolve route (any L; for L = 4 the fallback of dwest4_fast, out of
+// line so the rare path stays out of the hot loop's instruction-cache footprint).
+template <int L>
+__device__ __forceinline__ void dwest_jacobi_body(const double (&A)[L][L], const double (&md)[L], double frac,
+                                                  double& score, int& count) {
+    double vec[L][L], w[L];
+    dwest_eigen<L>(A, vec, w);
+    dwest_select<L>(frac, md, vec, w, score, count);
+}
+__device__ __noinline__ void dwest_jacobi4(const double (&A)[4][4], const double (&md)[4], double frac,
+                                           double& score, int& count) {
+    dwest_jacobi_body<4>(A, md, frac, score, count);
+}
+
+// ---- DWEST for 4 bands without a full eigendecomposition -----------------------------
+// Only the eigenpairs with lambda >= f lambda_max > 0 enter the score (one for ~83% of
+// the C5 pixels, two for ~16%, three for 0.03%), so the 4 x 4 problem is solved for the
+// top two pairs only, each to fp64 backward-stable accuracy (eps |A| / gap, like the
+// reference's QL iteration):
+//   1. scale by a power of two (exact) so max |a_ij| is in [1, 2);
+//   2. tridiagonalise: one Householder reflector (column 0) + one plane rotation;
+//   3. monic characteristic polynomial of the tridiagonal T; lambda_1 by Laguerre's
+//      iteration from the Gershgorin bound (monotone and cubically convergent for a
+//      real-rooted polynomial), lambda_2 the same way on the deflated cubic from
+//      lambda_1; each then polished by Newton steps on T's three-term recurrence (a
+//      backward-stable evaluation of det(T - x I), which the power-basis form is not);
+//   4. eigenvector of T by the twisted factorisation in product form: column k* of
+//      adj(T - lambda I) with the largest diagonal entry theta_k phi_{k+1} (leading and
+//      trailing principal minors), mapped back through the rotation and the reflector;
+//   5. sign rule, projection, count.
+// Pixels the two-pair route cannot settle — a third eigenvalue at or near the cutoff, a
+// selected eigenvalue closer than kDw4Gap (in units of |A|) to a neighbour, an iteration
+// that did not converge — take the general Jacobi route instead (a few 1e-4 of C5).
+constexpr double kDw4Gap = 3e-5;
+constexpr double kDw4LagTol = 1e-6;
+
+// sqrt of x >= 0 without the IEEE sqrt subroutine (0 -> 0)
+__device__ __forceinline__ double sqrt_pos(double x) { return __dmul_rn(x, fast_rsqrt(x + DBL_MIN)); }
+// One Laguerre step a = n p / (p' + w sqrt(D)) with D = p'^2 - n/(n-1) p p'' (so that
+// w = n - 1). Right of the largest root of a real-rooted monic polynomial p, p' > 0 and
+// the iteration descends monotonically, so the sign of the root is fixed. sqrt and the
+// quotient come straight from the MUFU seeds (~2^-20): an error of that size in a step
+// only shows up as a 1e-6 |a| error of the iterate, and the Newton polish on the
+// recurrence follows. D <= 0 (all roots equal, e.g. the zero matrix) gives NaN, which
+// fails every convergence test below: such pixels take the general route.
+__device__ __forceinline__ double laguerre_step(double p, double dp, double D, double w, double n) {
+    double rs, rc;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(D));
+    const double den = fma(__dmul_rn(D, w), rs, dp);
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+    return __dmul_rn(__dmul_rn(p, n), rc);
+}
+
+struct Tri4 {
+    double d[4], e[3], f[3];  // diagonal, off-diagonal, off-diagonal squared
+    double v0, v1, v2, beta;  // reflector on coordinates 1..3: H = I - beta v v^T
+    double c, s;              // rotation on coordinates 2, 3
+};
+
+// det(T - x I) and its derivative by the three-term recurrence
+__device__ __forceinline__ void tri4_eval(const Tri4& T, double x, double& p, double& dp) {
+    const double g0 = T.d[0] - x, g1 = T.d[1] - x, g2 = T.d[2] - x, g3 = T.d[3] - x;
+    const double t1 = g0;
+    const double t2 = fma(g1, t1, -T.f[0]);
+    const double u2 = -g1 - t1;                                // dt2 = g1 dt1 - t1, dt1 = -1
+    const double t3 = fma(g2, t2, __dmul_rn(-T.f[1], t1));
+    const double u3 = fma(g2, u2, T.f[1] - t2);                // g2 dt2 - t2 - f1 dt1
+    p = fma(g3, t3, __dmul_rn(-T.f[2], t2));
+    dp = fma(g3, u3, fma(-T.f[2], u2, -t3));
+}
+
+// Newton polish of an eigenvalue estimate on the recurrence; returns false when it did
+// not settle (a multiple root: the caller falls back)
+__device__ __forceinline__ bool tri4_polish(const Tri4& T, double& x) {
+    double st = 1.0;
+#pragma unroll 1
+    for (int it = 0; it < 4 && fabs(st) > 1e-9; ++it) {
+        double p, dp;
+        tri4_eval(T, x, p, dp);
+        st = dp != 0.0 ? __dmul_rn(p, fast_rcp(dp)) : 0.0;
+        x -= st;
+    }
+    return fabs(st) <= 1e-9;
+}
+
+// signed projection sigma (v . md) of T's eigenvector at lam, back in A's coordinates
+__device__ __forceinline__ double tri4_project(const Tri4& T, double lam, const double (&md)[4]) {
+    const double g0 = T.d[0] - lam, g1 = T.d[1] - lam, g2 = T.d[2] - lam, g3 = T.d[3] - lam;
+    const double th1 = g0;
+    const double th2 = fma(g1, th1, -T.f[0]);
+    const double th3 = fma(g2, th2, __dmul_rn(-T.f[1], th1));
+    const double ph3 = g3;
+    const double ph2 = fma(g2, ph3, -T.f[2]);
+    const double ph1 = fma(g1, ph2, __dmul_rn(-T.f[1], ph3));
+    // adj(T - lam I), upper triangle
+    const double t01 = __dmul_rn(T.e[0], T.e[1]), t12 = __dmul_rn(T.e[1], T.e[2]);
+    const double h1 = __dmul_rn(th1, T.e[1]);
+    const double a00 = ph1, a11 = __dmul_rn(th1, ph2), a22 = __dmul_rn(th2, ph3), a33 = th3;
+    const double a01 = __dmul_rn(-T.e[0], ph2), a02 = __dmul_rn(t01, ph3), a03 = __dmul_rn(-t01, T.e[2]);
+    const double a12 = __dmul_rn(-h1, ph3), a13 = __dmul_rn(th1, t12), a23 = __dmul_rn(-th2, T.e[2]);
+    // the column with the largest diagonal entry (the twist index)
+    double best = fabs(a00), z0 = a00, z1 = a01, z2 = a02, z3 = a03;
+    bool b = fabs(a11) > best;
+    best = b ? fabs(a11) : best;
+    z0 = b ? a01 : z0, z1 = b ? a11 : z1, z2 = b ? a12 : z2, z3 = b ? a13 : z3;
+    b = fabs(a22) > best;
+    best = b ? fabs(a22) : best;
+    z0 = b ? a02 : z0, z1 = b ? a12 : z1, z2 = b ? a22 : z2, z3 = b ? a23 : z3;
+    b = fabs(a33) > best;
+    z0 = b ? a03 : z0, z1 = b ? a13 : z1, z2 = b ? a23 : z2, z3 = b ? a33 : z3;
+    // back through the rotation (coordinates 2, 3) and the reflector (coordinates 1..3)
+    const double y2 = fma(T.c, z2, __dmul_rn(-T.s, z3));
+    const double y3 = fma(T.s, z2, __dmul_rn(T.c, z3));
+    const double tt = __dmul_rn(T.beta, fma(T.v2, y3, fma(T.v1, y2, __dmul_rn(T.v0, z1))));
+    const double x0 = z0, x1 = fma(-tt, T.v0, z1), x2 = fma(-tt, T.v1, y2), x3 = fma(-tt, T.v2, y3);
+    const double n2 = fma(x3, x3, fma(x2, x2, fma(x1, x1, __dmul_rn(x0, x0))));
+    const double dot = fma(x3, md[3], fma(x2, md[2], fma(x1, md[1], __dmul_rn(x0, md[0]))));
+    // sign rule: the first largest-|.| component positive
+    double lead = x0, bl = fabs(x0);
+    b = fabs(x1) > bl;
+    lead = b ? x1 : lead, bl = b ? fabs(x1) : bl;
+    b = fabs(x2) > bl;
+    lead = b ? x2 : lead, bl = b ? fabs(x2) : bl;
+    lead = fabs(x3) > bl ? x3 : lead;
+    const double pr = __dmul_rn(dot, fast_rsqrt(n2 + DBL_MIN));
+    return lead < 0.0 ? -pr : pr;
+}
+
+// Returns false when the pixel needs the general route.
+__device__ __forceinline__ bool dwest4_fast(const double (&A)[4][4], const double (&md)[4], double frac,
+                                            double& score, int& count) {
+    // 1. exact power-of-two scaling: max |a_ij| -> [1, 2)
+    unsigned hmax = 0u;  // only the exponent of max |a_ij| matters: compare the high words
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j < 4; ++j) hmax = max(hmax, static_cast<unsigned>(__double2hiint(A[i][j])) & 0x7fffffffu);
+    const int ex = static_cast<int>(hmax >> 20);
+    const double sc = __hiloint2double((2046 - ex) << 20, 0);
+    const double a00 = A[0][0] * sc, a01 = A[0][1] * sc, a02 = A[0][2] * sc, a03 = A[0][3] * sc;
+    const double a11 = A[1][1] * sc, a12 = A[1][2] * sc, a13 = A[1][3] * sc;
+    const double a22 = A[2][2] * sc, a23 = A[2][3] * sc, a33 = A[3][3] * sc;
+    // 2. tridiagonal form
+    Tri4 T;
+    {
+        const double nx = sqrt_pos(fma(a03, a03, fma(a02, a02, __dmul_rn(a01, a01))));
+        const double alpha = a01 >= 0.0 ? -nx : nx;
+        T.v0 = a01 - alpha, T.v1 = a02, T.v2 = a03;
+        const double vv = fma(T.v2, T.v2, fma(T.v1, T.v1, __dmul_rn(T.v0, T.v0)));
+        T.beta = vv > 0.0 ? 2.0 * fast_rcp(vv) : 0.0;
+        const double p0 = __dmul_rn(T.beta, fma(a13, T.v2, fma(a12, T.v1, __dmul_rn(a11, T.v0))));
+        const double p1 = __dmul_rn(T.beta, fma(a23, T.v2, fma(a22, T.v1, __dmul_rn(a12, T.v0))));
+        const double p2 = __dmul_rn(T.beta, fma(a33, T.v2, fma(a23, T.v1, __dmul_rn(a13, T.v0))));
+        const double K = __dmul_rn(0.5 * T.beta, fma(T.v2, p2, fma(T.v1, p1, __dmul_rn(T.v0, p0))));
+        const double w0 = fma(-K, T.v0, p0), w1 = fma(-K, T.v1, p1), w2 = fma(-K, T.v2, p2);
+        const double b11 = fma(-2.0 * T.v0, w0, a11);
+        const double b12 = fma(-w0, T.v1, fma(-T.v0, w1, a12));
+        const double b13 = fma(-w0, T.v2, fma(-T.v0, w2, a13));
+        const double b22 = fma(-2.0 * T.v1, w1, a22);
+        const double b23 = fma(-w1, T.v2, fma(-T.v1, w2, a23));
+        const double b33 = fma(-2.0 * T.v2, w2, a33);
+        T.d[0] = a00, T.e[0] = alpha, T.d[1] = b11;
+        const double r2 = fma(b13, b13, __dmul_rn(b12, b12));
+        const double rinv = fast_rsqrt(r2 + DBL_MIN);
+        T.c = r2 > 0.0 ? __dmul_rn(b12, rinv) : 1.0;
+        T.s = r2 > 0.0 ? __dmul_rn(b13, rinv) : 0.0;
+        T.e[1] = __dmul_rn(r2, rinv);
+        const double cc = __dmul_rn(T.c, T.c), ss = __dmul_rn(T.s, T.s), cs2 = __dmul_rn(2.0 * T.c, T.s);
+        T.d[2] = fma(ss, b33, fma(cs2, b23, __dmul_rn(cc, b22)));
+        T.d[3] = fma(cc, b33, fma(-cs2, b23, __dmul_rn(ss, b22)));
+        T.e[2] = fma(0.5 * cs2, b33 - b22, __dmul_rn(cc - ss, b23));
+#pragma unroll
+        for (int i = 0; i < 3; ++i) T.f[i] = __dmul_rn(T.e[i], T.e[i]);
+    }
+    // 3. monic characteristic polynomial x^4 + c3 x^3 + c2 x^2 + c1 x + c0
+    const double p21 = -(T.d[0] + T.d[1]), p20 = fma(T.d[0], T.d[1], -T.f[0]);
+    const double p32 = p21 - T.d[2];
+    const double p31 = fma(-T.d[2], p21, p20 - T.f[1]);
+    const double p30 = fma(T.f[1], T.d[0], __dmul_rn(-T.d[2], p20));
+    const double c3 = p32 - T.d[3];
+    const double c2 = fma(-T.d[3], p32, p31 - T.f[2]);
+    const double c1 = fma(-T.f[2], p21, fma(-T.d[3], p31, p30));
+    const double c0 = fma(-T.f[2], p20, __dmul_rn(-T.d[3], p30));
+    //    lambda_1: Laguerre from the Gershgorin upper bound
+    const double ae0 = fabs(T.e[0]), ae2 = fabs(T.e[2]);  // e[1] >= 0
+    double x = max_sel(max_sel(T.d[0] + ae0, T.d[1] + (ae0 + T.e[1])), max_sel(T.d[2] + (T.e[1] + ae2), T.d[3] + ae2));
+    bool ok = true;
+    {
+        const double k3 = 3.0 * c3, k2 = 2.0 * c2;
+        double a = 1.0;
+        int it = 0;
+#pragma unroll 1
+        for (; it < 12 && fabs(a) > kDw4LagTol; ++it) {
+            const double p = fma(fma(fma(x + c3, x, c2), x, c1), x, c0);
+            const double dp = fma(fma(fma(4.0, x, k3), x, k2), x, c1);
+            const double hp = fma(fma(6.0, x, k3), x, c2);  // p'' / 2
+            // a = n p / (p' + sqrt((n-1)((n-1) p'^2 - n p p''))), n = 4
+            a = laguerre_step(p, dp, fma(__dmul_rn(p, -8.0 / 3.0), hp, __dmul_rn(dp, dp)), 3.0, 4.0);
+            x -= a;
+        }
+        ok = fabs(a) <= kDw4LagTol;
+    }
+    double lam1 = x;
+    ok = tri4_polish(T, lam1) && ok;
+    score = 0.0;
+    count = 0;
+    if (!(lam1 > 0.0)) return ok;  // no positive eigenvalue: score 0 (detect.cpp:254)
+    //    lambda_2 on the deflated cubic x^3 + q2 x^2 + q1 x + q0, from lambda_1
+    const double q2 = c3 + lam1, q1 = fma(lam1, q2, c2), q0 = fma(lam1, q1, c1);
+    {
+        const double k2 = 2.0 * q2;
+        double a = 1.0;
+        int it = 0;
+        x = lam1;
+#pragma unroll 1
+        for (; it < 12 && fabs(a) > kDw4LagTol; ++it) {
+            const double p = fma(fma(x + q2, x, q1), x, q0);
+            const double dp = fma(fma(3.0, x, k2), x, q1);
+            const double hp = fma(3.0, x, q2);  // p'' / 2
+            a = laguerre_step(p, dp, fma(__dmul_rn(p, -3.0), hp, __dmul_rn(dp, dp)), 2.0, 3.0);  // n = 3
+            x -= a;
+        }
+        ok = ok && fabs(a) <= kDw4LagTol;
+    }
+    double lam2 = x;
+    ok = tri4_polish(T, lam2) && ok;
+    //    lambda_3 from the remaining quadratic x^2 + r1 x + r0 (only its distance to the
+    //    cutoff and to lambda_2 matters)
+    const double r1 = q2 + lam2, r0 = fma(lam2, r1, q1);
+    const double lam3 = 0.5 * (sqrt_pos(fmax(fma(r1, r1, -4.0 * r0), 0.0)) - r1);
+    const double cut = __dmul_rn(frac, lam1);
+    const bool take2 = lam2 > 0.0 && !(lam2 < cut);
+    // the two-pair route settles the pixel when lambda_3 is clearly below the cutoff and
+    // every selected eigenvalue is clear of its neighbours
+    ok = ok && lam3 < cut - fma(1e-6, cut, 1e-9) && lam1 - lam2 >= kDw4Gap && (!take2 || lam2 - lam3 >= kDw4Gap);
+    // 4./5. eigenvectors, sign rule, projection
+    double proj = tri4_project(T, lam1, md);
+    if (take2) proj += tri4_project(T, lam2, md);
+    score = fabs(proj);
+    count = take2 ? 2 : 1;
+    return ok;
+}
+
+// DWEST score and eigen-count of one pixel from C_in - C_ann and m_in - m_ann
+template <int L>
+__device__ __forceinline__ void dwest_score(const double (&A)[L][L], const double (&md)[L], double frac,
+                                            double& score, int& count) {
+    if constexpr (L == 4) {
+#ifndef HSAD_DWEST_JACOBI
+        if (!dwest4_fast(A, md, frac, score, count))
+#endif
+            dwest_jacobi4(A, md, frac, score, count);
+    } else {
+        dwest_jacobi_body<L>(A, md, frac, score, count);
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>& D, int64_t o) {
+    double score;
+    int count;
+    dwest_score<L>(D.cd, D.md, R.frac, score, count);
     store_score(R, o, score);
     if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
 }
@@ -912,11 +1179,11 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
     const bool bg_zero = ZC && cnt0 - nzc == 0;
     double muL[L], cm[L][L], dv[L];
     mean_cov<L>(bg, RL.n_a, muL, cm, false);
-    double dmaxL = 0.0;
+    bool dnzL = false;
 #pragma unroll
     for (int i = 0; i < L; ++i) {
         dv[i] = yc[i] - muL[i];
-        dmaxL = fmax(dmaxL, fabs(dv[i]));
+        dnzL = dnzL | (fabs(dv[i]) > 0.0);
     }
     DualStats<L> D;
     dual_stats<L>(S1, S0, P.n_in, P.n_ann, ZC && cnt1 == 0, ZC && cnt0 - cnt1 == 0, D);
@@ -929,17 +1196,13 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
     double scoreL = 0.0, deltaL = 0.0, scoreR = 0.0, deltaR = 0.0;
     int codeL = chol_quad<L>(cm, dv, RL.ridge, scoreL, deltaL);
     int codeR = chol_quad<L>(a, D.md, RR.ridge, scoreR, deltaR);
-    float v32[L][L];
-    // the sweeps stay a loop: unrolled, the kernel outgrows the instruction cache
-    // (measured 4.6% slower on the C5 sweep)
-    dwest_f32_stage<L>(D.cd, v32);
     // LRX epilogue (lrx_solve)
     if (bg_zero) {
         if (nzc) report(P, qL, r, col, HSAD_E_SINGULAR_AFTER_RIDGE);
         store_score(RL, o, 0.0);
     } else {
         double score = 0.0;
-        if (dmaxL > 0.0) {
+        if (dnzL) {
             if (lin == P.diag_lin && P.req_base + qL == P.diag_req) *P.diag_out = deltaL;
             score = scoreL;
             if (codeL == kIllConditioned) {
@@ -956,7 +1219,7 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
     // DWRX epilogue (dwrx_solve)
     {
         double score = 0.0;
-        if (D.mmax > 0.0) {
+        if (D.mnz) {
             if (lin == P.diag_lin && P.req_base + qR == P.diag_req) *P.diag_out = deltaR;
             score = scoreR;
             if (codeR == kIllConditioned) {
@@ -971,9 +1234,11 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
         store_score(RR, o, fabs(score));
     }
     // DWEST (dwest_solve)
-    double vec[L][L], w[L];
-    dwest_f64_stage<L>(D.cd, v32, vec, w);
-    dwest_select<L>(RE, D, vec, w, o);
+#ifdef HSAD_EXP_NODWEST  // experiment: the kernel without the eigensolve (lower bound)
+    store_score(RE, o, D.cd[0][0]);
+#else
+    dwest_solve<L>(RE, D, o);
+#endif
 }
 
 // Per-pixel solves of every request from the box sums S (detect.cpp:168-271).
@@ -1554,10 +1819,14 @@ cudaError_t launch_lk(const DetectParams& P, dim3 grid, int nt, int kcols, cudaS
 template <int L>
 cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, int kcols, cudaStream_t s) {
     switch (P.nbox) {
+#ifndef HSAD_FAST_BUILD  // A/B builds of the C5 sweep kernel only (scripts/build_variant.sh)
         case 1: return launch_lk<L, 1>(P, grid, nt, kcols, s);
+#endif
         case 2: return launch_lk<L, 2>(P, grid, nt, kcols, s);
+#ifndef HSAD_FAST_BUILD
         case 3: return launch_lk<L, 3>(P, grid, nt, kcols, s);
         case 4: return launch_lk<L, 4>(P, grid, nt, kcols, s);
+#endif
     }
     return cudaErrorInvalidValue;
 }
@@ -1565,14 +1834,18 @@ cudaError_t launch_l(const DetectParams& P, dim3 grid, int nt, int kcols, cudaSt
 cudaError_t launch_bands(int bands, const DetectParams& P, dim3 grid, int nt, int kcols,
                          cudaStream_t s) {
     switch (bands) {
+#ifndef HSAD_FAST_BUILD
         case 1: return launch_l<1>(P, grid, nt, kcols, s);
         case 2: return launch_l<2>(P, grid, nt, kcols, s);
         case 3: return launch_l<3>(P, grid, nt, kcols, s);
+#endif
         case 4: return launch_l<4>(P, grid, nt, kcols, s);
+#ifndef HSAD_FAST_BUILD
         case 5: return launch_l<5>(P, grid, nt, kcols, s);
         case 6: return launch_l<6>(P, grid, nt, kcols, s);
         case 7: return launch_l<7>(P, grid, nt, kcols, s);
         case 8: return launch_l<8>(P, grid, nt, kcols, s);
+#endif
     }
     return cudaErrorInvalidValue;
 }
