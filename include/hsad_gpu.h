@@ -168,6 +168,16 @@ hsad_status hsad_detect(const void* d_cube, int32_t elem_bytes, int64_t lines, i
                         int32_t bands, const hsad_detect_request* request,
                         hsad_pixel_error* err, void* stream);
 
+/* symmetric_eigen + the DWEST selection loop (stats.cpp:64-89, detect.cpp:252-263) on a
+ * batch of n 4 x 4 symmetric matrices: d_cdiff n*16 doubles (row-major; the upper triangle
+ * is read), d_mdiff n*4. d_scores[i] = |sum over {lambda_j > 0, lambda_j >= f lambda_max} of
+ * v_j . m_diff| with the sign rule of stats.cpp:83-85, d_counts[i] (optional) the size of that
+ * set, d_route[i] (optional) 0 when the two-pair tridiagonal route settled the matrix and 1
+ * when it went through the general Jacobi route. The device code is the fused detectors'. */
+hsad_status hsad_dwest_pairs(const double* d_cdiff, const double* d_mdiff, int64_t n,
+                             double eigen_fraction, double* d_scores, int8_t* d_counts,
+                             int8_t* d_route, void* stream);
+
 /* Fused multi-detector over a row strip. The image is `lines` x `samples` x
  * `bands`; the buffer d_cube holds global rows [buf_row0, buf_row0 + buf_rows)
  * (row strip plus mirror halo; hsad_strip_rows() computes the range) and the

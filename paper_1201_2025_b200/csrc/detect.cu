@@ -562,7 +562,11 @@ __device__ __forceinline__ void dwest_f32_stage(const double (&A)[L][L], float (
 }
 
 // Stage 2 (fp64): Gram-Schmidt of the fp32 vectors, B = Q^T A Q, polish sweeps.
-template <int L>
+// EXTRA: one more sweep after the off-diagonal test passes. The test is relative to |B|, so a
+// pair of eigenvalues much closer than |B| keeps a rotation error of ~1e-12 |B| / gap; the
+// 4-band fallback route, which exists for exactly such pairs, takes the extra (quadratically
+// convergent) sweep.
+template <int L, bool EXTRA = false>
 __device__ __forceinline__ void dwest_f64_stage(const double (&A)[L][L], const float (&v32)[L][L],
                                                 double (&V)[L][L], double (&w)[L]) {
     // modified Gram-Schmidt in fp64
@@ -627,15 +631,16 @@ __device__ __forceinline__ void dwest_f64_stage(const double (&A)[L][L], const f
             if (__all_sync(__activemask(), off <= 1e-24 * dia)) break;
         }
     }
+    if constexpr (EXTRA) sweep64<L>(B, V);
 #pragma unroll
     for (int i = 0; i < L; ++i) w[i] = B[i][i];
 }
 
-template <int L>
+template <int L, bool EXTRA = false>
 __device__ __forceinline__ void dwest_eigen(const double (&A)[L][L], double (&V)[L][L], double (&w)[L]) {
     float v32[L][L];
     dwest_f32_stage<L>(A, v32);
-    dwest_f64_stage<L>(A, v32, V, w);
+    dwest_f64_stage<L, EXTRA>(A, v32, V, w);
 }
 
 __device__ __forceinline__ void store_score(const ReqDev& R, int64_t o, double s) {
@@ -875,7 +880,7 @@ template <int L>
 __device__ __forceinline__ void dwest_jacobi_body(const double (&A)[L][L], const double (&md)[L], double frac,
                                                   double& score, int& count) {
     double vec[L][L], w[L];
-    dwest_eigen<L>(A, vec, w);
+    dwest_eigen<L, L == 4>(A, vec, w);
     dwest_select<L>(frac, md, vec, w, score, count);
 }
 __device__ __noinline__ void dwest_jacobi4(const double (&A)[4][4], const double (&md)[4], double frac,
@@ -997,10 +1002,8 @@ __device__ __forceinline__ double tri4_project(const Tri4& T, double lam, const 
     return lead < 0.0 ? -pr : pr;
 }
 
-// Returns false when the pixel needs the general route.
-__device__ __forceinline__ bool dwest4_fast(const double (&A)[4][4], const double (&md)[4], double frac,
-                                            double& score, int& count) {
-    // 1. exact power-of-two scaling: max |a_ij| -> [1, 2)
+// 1. exact power-of-two scaling: max |a_ij| -> [1, 2) (upper triangle)
+__device__ __forceinline__ void dwest4_scale(const double (&A)[4][4], double (&S)[4][4]) {
     unsigned hmax = 0u;  // only the exponent of max |a_ij| matters: compare the high words
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -1008,9 +1011,18 @@ __device__ __forceinline__ bool dwest4_fast(const double (&A)[4][4], const doubl
         for (int j = i; j < 4; ++j) hmax = max(hmax, static_cast<unsigned>(__double2hiint(A[i][j])) & 0x7fffffffu);
     const int ex = static_cast<int>(hmax >> 20);
     const double sc = __hiloint2double((2046 - ex) << 20, 0);
-    const double a00 = A[0][0] * sc, a01 = A[0][1] * sc, a02 = A[0][2] * sc, a03 = A[0][3] * sc;
-    const double a11 = A[1][1] * sc, a12 = A[1][2] * sc, a13 = A[1][3] * sc;
-    const double a22 = A[2][2] * sc, a23 = A[2][3] * sc, a33 = A[3][3] * sc;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j < 4; ++j) S[i][j] = A[i][j] * sc;
+}
+
+// A: the scaled matrix (dwest4_scale). Returns false when the pixel needs the general route.
+__device__ __forceinline__ bool dwest4_fast(const double (&A)[4][4], const double (&md)[4], double frac,
+                                            double& score, int& count) {
+    const double a00 = A[0][0], a01 = A[0][1], a02 = A[0][2], a03 = A[0][3];
+    const double a11 = A[1][1], a12 = A[1][2], a13 = A[1][3];
+    const double a22 = A[2][2], a23 = A[2][3], a33 = A[3][3];
     // 2. tridiagonal form
     Tri4 T;
     {
@@ -1117,10 +1129,14 @@ template <int L>
 __device__ __forceinline__ void dwest_score(const double (&A)[L][L], const double (&md)[L], double frac,
                                             double& score, int& count) {
     if constexpr (L == 4) {
+        // both routes see the scaled matrix: eigenvectors and the selection are scale-free,
+        // and neither route then under- or overflows on tiny or huge covariances
+        double S[4][4];
+        dwest4_scale(A, S);
 #ifndef HSAD_DWEST_JACOBI
-        if (!dwest4_fast(A, md, frac, score, count))
+        if (!dwest4_fast(S, md, frac, score, count))
 #endif
-            dwest_jacobi4(A, md, frac, score, count);
+            dwest_jacobi4(S, md, frac, score, count);
     } else {
         dwest_jacobi_body<L>(A, md, frac, score, count);
     }
@@ -1133,6 +1149,34 @@ __device__ __forceinline__ void dwest_solve(const ReqDev& R, const DualStats<L>&
     dwest_score<L>(D.cd, D.md, R.frac, score, count);
     store_score(R, o, score);
     if (R.eigcount) R.eigcount[o] = static_cast<int8_t>(count);
+}
+
+// symmetric_eigen + the DWEST selection loop (stats.cpp:64-89, detect.cpp:252-263) on a
+// batch of 4 x 4 matrices: one thread per (C_diff, m_diff) pair, the same device code
+// path as the fused detector (hsad_dwest_pairs).
+__global__ void dwest_pairs_kernel(const double* __restrict__ cdiff, const double* __restrict__ mdiff,
+                                   int64_t n, double frac, double* __restrict__ scores,
+                                   int8_t* __restrict__ counts, int8_t* __restrict__ route) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double A[4][4], md[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        md[r] = mdiff[i * 4 + r];
+#pragma unroll
+        for (int c = r; c < 4; ++c) A[r][c] = cdiff[i * 16 + r * 4 + c];  // upper triangle
+    }
+    double score, S[4][4];
+    int count;
+    dwest4_scale(A, S);
+    bool fast = dwest4_fast(S, md, frac, score, count);
+#ifdef HSAD_DWEST_JACOBI
+    fast = false;
+#endif
+    if (!fast) dwest_jacobi4(S, md, frac, score, count);
+    scores[i] = score;
+    if (counts) counts[i] = static_cast<int8_t>(count);
+    if (route) route[i] = fast ? 0 : 1;
 }
 
 template <int NBOX>
@@ -2446,6 +2490,22 @@ hsad_status hsad_detect(const void* d_cube, int32_t elem_bytes, int64_t lines, i
                         void* stream) {
     return detect_multi_impl(d_cube, elem_bytes, lines, samples, bands, 0, lines, 0, lines,
                              request, 1, nullptr, err, static_cast<cudaStream_t>(stream));
+}
+
+hsad_status hsad_dwest_pairs(const double* d_cdiff, const double* d_mdiff, int64_t n,
+                             double eigen_fraction, double* d_scores, int8_t* d_counts,
+                             int8_t* d_route, void* stream) {
+    if (n < 0 || (n > 0 && (!d_cdiff || !d_mdiff || !d_scores)))
+        return set_error(HSAD_E_INVALID_VALUE, "null buffer");
+    if (!(eigen_fraction > 0.0 && eigen_fraction <= 1.0))
+        return set_error(HSAD_E_INVALID_VALUE, "eigen fraction must be in (0, 1]");
+    if (hsad_device_check() != HSAD_OK) return HSAD_E_CUDA;
+    if (n == 0) return HSAD_OK;
+    const int nt = 128;
+    dwest_pairs_kernel<<<static_cast<unsigned>((n + nt - 1) / nt), nt, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_cdiff, d_mdiff, n, eigen_fraction, d_scores, d_counts, d_route);
+    const cudaError_t ce = cudaGetLastError();
+    return ce == cudaSuccess ? HSAD_OK : set_error(HSAD_E_CUDA, cudaGetErrorString(ce));
 }
 
 }  // extern "C"

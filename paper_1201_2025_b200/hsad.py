@@ -321,6 +321,27 @@ def dwest(cube: torch.Tensor, config: WindowConfig, dcfg: DwestConfig | float = 
     return m
 
 
+def dwest_pairs(cdiff: torch.Tensor, mdiff: torch.Tensor, eigen_fraction: float = 0.1):
+    """symmetric_eigen + the DWEST selection (stats.cpp:64-89, detect.cpp:252-263) on a batch
+    of 4 x 4 matrices: cdiff (n, 4, 4) fp64 symmetric, mdiff (n, 4) fp64, CUDA tensors.
+    Returns (scores fp64 (n,), counts int8 (n,), route int8 (n,): 0 = two-pair route,
+    1 = general Jacobi route). The device code is the fused detectors'."""
+    cdiff = _require_cuda(cdiff, "cdiff")
+    mdiff = _require_cuda(mdiff, "mdiff")
+    if cdiff.dtype != torch.float64 or mdiff.dtype != torch.float64:
+        raise TypeError("dwest_pairs takes float64 tensors")
+    n = cdiff.shape[0]
+    if tuple(cdiff.shape[1:]) != (4, 4) or tuple(mdiff.shape) != (n, 4):
+        raise ValueError("cdiff must be (n, 4, 4) and mdiff (n, 4)")
+    scores = torch.empty(n, dtype=torch.float64, device=cdiff.device)
+    counts = torch.empty(n, dtype=torch.int8, device=cdiff.device)
+    route = torch.empty(n, dtype=torch.int8, device=cdiff.device)
+    _check(_abi.lib().hsad_dwest_pairs(cdiff.data_ptr(), mdiff.data_ptr(), n, float(eigen_fraction),
+                                       scores.data_ptr(), counts.data_ptr(), route.data_ptr(),
+                                       _stream_ptr()))
+    return scores, counts, route
+
+
 def detect(cube: torch.Tensor, algorithm: str, config: WindowConfig,
            options: DetectOptions = DetectOptions()) -> ScoreMap:
     """hsad::detect dispatch (detect.cpp:278-289)."""
