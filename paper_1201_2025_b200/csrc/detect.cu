@@ -57,6 +57,7 @@ hsad_status fullband_dwest_launch(FbParams& P, cudaStream_t s);
 namespace {
 
 constexpr int kCodeOverflow = 0x80;
+
 // Boxes of at least this radius use the lane-pair horizontal sums (K = 1 kernels)
 #ifndef HSAD_PAIR_RADIUS
 #define HSAD_PAIR_RADIUS 2
@@ -883,9 +884,12 @@ __device__ __forceinline__ void dwest_jacobi_body(const double (&A)[L][L], const
     dwest_eigen<L, L == 4>(A, vec, w);
     dwest_select<L>(frac, md, vec, w, score, count);
 }
+__device__ __forceinline__ void dwest4_scale(const double (&A)[4][4], double (&S)[4][4]);
 __device__ __noinline__ void dwest_jacobi4(const double (&A)[4][4], const double (&md)[4], double frac,
                                            double& score, int& count) {
-    dwest_jacobi_body<4>(A, md, frac, score, count);
+    double S[4][4];  // the power-of-two-scaled matrix, like the two-pair route: eigenvectors and the
+    dwest4_scale(A, S);  // selection are scale-free, and tiny or huge covariances neither under- nor overflow
+    dwest_jacobi_body<4>(S, md, frac, score, count);
 }
 
 // ---- DWEST for 4 bands without a full eigendecomposition -----------------------------
@@ -1017,12 +1021,14 @@ __device__ __forceinline__ void dwest4_scale(const double (&A)[4][4], double (&S
         for (int j = i; j < 4; ++j) S[i][j] = A[i][j] * sc;
 }
 
-// A: the scaled matrix (dwest4_scale). Returns false when the pixel needs the general route.
+// Returns false when the pixel needs the general route.
 __device__ __forceinline__ bool dwest4_fast(const double (&A)[4][4], const double (&md)[4], double frac,
                                             double& score, int& count) {
-    const double a00 = A[0][0], a01 = A[0][1], a02 = A[0][2], a03 = A[0][3];
-    const double a11 = A[1][1], a12 = A[1][2], a13 = A[1][3];
-    const double a22 = A[2][2], a23 = A[2][3], a33 = A[3][3];
+    double S[4][4];
+    dwest4_scale(A, S);
+    const double a00 = S[0][0], a01 = S[0][1], a02 = S[0][2], a03 = S[0][3];
+    const double a11 = S[1][1], a12 = S[1][2], a13 = S[1][3];
+    const double a22 = S[2][2], a23 = S[2][3], a33 = S[3][3];
     // 2. tridiagonal form
     Tri4 T;
     {
@@ -1129,14 +1135,10 @@ template <int L>
 __device__ __forceinline__ void dwest_score(const double (&A)[L][L], const double (&md)[L], double frac,
                                             double& score, int& count) {
     if constexpr (L == 4) {
-        // both routes see the scaled matrix: eigenvectors and the selection are scale-free,
-        // and neither route then under- or overflows on tiny or huge covariances
-        double S[4][4];
-        dwest4_scale(A, S);
 #ifndef HSAD_DWEST_JACOBI
-        if (!dwest4_fast(S, md, frac, score, count))
+        if (!dwest4_fast(A, md, frac, score, count))
 #endif
-            dwest_jacobi4(S, md, frac, score, count);
+            dwest_jacobi4(A, md, frac, score, count);
     } else {
         dwest_jacobi_body<L>(A, md, frac, score, count);
     }
@@ -1166,14 +1168,13 @@ __global__ void dwest_pairs_kernel(const double* __restrict__ cdiff, const doubl
 #pragma unroll
         for (int c = r; c < 4; ++c) A[r][c] = cdiff[i * 16 + r * 4 + c];  // upper triangle
     }
-    double score, S[4][4];
+    double score;
     int count;
-    dwest4_scale(A, S);
-    bool fast = dwest4_fast(S, md, frac, score, count);
+    bool fast = dwest4_fast(A, md, frac, score, count);
 #ifdef HSAD_DWEST_JACOBI
     fast = false;
 #endif
-    if (!fast) dwest_jacobi4(S, md, frac, score, count);
+    if (!fast) dwest_jacobi4(A, md, frac, score, count);
     scores[i] = score;
     if (counts) counts[i] = static_cast<int8_t>(count);
     if (route) route[i] = fast ? 0 : 1;
@@ -1580,9 +1581,10 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
     for (int64_t r = ra; r < rb; ++r) {
         // K = 1: fetch the centre spectrum first; its latency hides behind the
         // vertical update, the barrier and the horizontal sums
+        // (raw values: the shift and the zero test wait until the spectrum is used, so
+        // the load is in flight across the update and the barrier)
         double yc1[L];
-        int nzc1 = 0;
-        if (owner1) nzc1 = shifted(own_cb, r, yc1);
+        if (owner1) load_row<L, STD, FUSE>(P, own_cb, row_bytes, static_cast<int>(r), yc1);
         if (r > ra) {
             if constexpr (STD) {
                 mbar_wait(&s_bar, st_phase);
@@ -1716,6 +1718,11 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
                 }
                 cnt[k] = ck;
             }
+            // K = 1: the window sums are in registers and nothing below reads the shared
+            // vertical sums, so the row's second barrier sits here, where the warps arrive
+            // together, and a warp that finishes its solves early goes straight on to the next
+            // row's update (its own columns) while the others still solve.
+            if constexpr (K == 1 && !FUSE) __syncthreads();
 #pragma unroll 1
             for (int j = 0; j < K; ++j) {
                 const int sc = seg0 + j;
@@ -1742,7 +1749,9 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
                 if (K == 1) {
 #pragma unroll
                     for (int i = 0; i < L; ++i) yc[i] = yc1[i];
-                    nzc = nzc1;
+                    nzc = nonzero<L>(yc);
+#pragma unroll
+                    for (int i = 0; i < L; ++i) yc[i] -= shift[i];
                 } else {
                     nzc = shifted(colbase_of(P.rmax + sc), r, yc);
                 }
@@ -1756,9 +1765,10 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
                 fused_dwt_row(P, wsm, mirror32(static_cast<int>(r + 2 + P.radius[0]), static_cast<int>(P.lines)),
                               c0, ncol);
         }
-        __syncthreads();
+        if constexpr (K > 1 || FUSE) __syncthreads();
         PT_MARK(4);  // barrier B
     }
+    if constexpr (K == 1 && !FUSE) __syncthreads();  // s_zero_seen of the last row's solves
     if constexpr (!ZC) {
         if (t == 0 && s_zero_seen && P.zflag)
             P.zflag[static_cast<int64_t>(by) * nbx + bx] = 1;
