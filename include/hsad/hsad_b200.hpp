@@ -20,8 +20,11 @@
 
 #include <chrono>
 #include <cstdint>
+#include <filesystem>
+#include <fstream>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "hsad_gpu.h"
@@ -290,6 +293,74 @@ inline ScoreMap detect(const HyperCube& cube, Algorithm algo, const WindowConfig
         case Algorithm::DWEST: return dwest(cube, config, options.dwest, options.workers);
     }
     throw Error(errc::invalid_value, "InvalidValue: unknown algorithm");
+}
+
+/// dual_window_samples (detect.cpp:150-157): the inner-box and annulus sample sets of one
+/// pixel, gathered on the GPU. `vectors` is dimension x count, column-major (the layout of the
+/// reference's Eigen::MatrixXd): sample i is vectors[i*dimension .. (i+1)*dimension).
+struct SampleSet {
+    int dim = 0;
+    std::vector<double> vectors;
+    int count() const { return dim ? static_cast<int>(vectors.size() / dim) : 0; }
+    int dimension() const { return dim; }
+    const double* col(int i) const { return vectors.data() + static_cast<size_t>(i) * dim; }
+};
+
+inline std::pair<SampleSet, SampleSet> dual_window_samples(const HyperCube& cube, int row, int col,
+                                                           const WindowConfig& config) {
+    detail::require_mode(config, WindowConfig::Mode::Dual, "dual_window_samples");
+    const int L = cube.bands();
+    const size_t n_in = static_cast<size_t>(config.inner_size) * config.inner_size;
+    const size_t n_out = static_cast<size_t>(config.outer_size) * config.outer_size - n_in;
+    SampleSet inner, outer;
+    inner.dim = outer.dim = L;
+    inner.vectors.resize(n_in * L);
+    outer.vectors.resize(n_out * L);
+    detail::DeviceBuffer din(cube.values.size() * sizeof(double)), di(inner.vectors.size() * sizeof(double)),
+        dout(outer.vectors.size() * sizeof(double));
+    detail::cuda(cudaMemcpy(din.p, cube.values.data(), cube.values.size() * sizeof(double), cudaMemcpyHostToDevice),
+         "H2D");
+    const hsad_window w = config.to_c();
+    detail::check(hsad_dual_window_samples(din.p, 8, cube.lines(), cube.samples(), L, row, col, &w,
+                                   static_cast<double*>(di.p), static_cast<double*>(dout.p), nullptr));
+    detail::cuda(cudaMemcpy(inner.vectors.data(), di.p, inner.vectors.size() * sizeof(double), cudaMemcpyDeviceToHost),
+         "D2H");
+    detail::cuda(cudaMemcpy(outer.vectors.data(), dout.p, outer.vectors.size() * sizeof(double), cudaMemcpyDeviceToHost),
+         "D2H");
+    return {std::move(inner), std::move(outer)};
+}
+
+/// save_score_map (detect.cpp:291-318): <prefix>.hdr (the text of write_envi_header,
+/// cube.cpp:184-196) and <prefix>.raw (1 band, BSQ, data type 4, little-endian); the fp32
+/// payload is encoded on the GPU (hsad_encode_score_map).
+inline void save_score_map(const ScoreMap& map, const std::filesystem::path& prefix) {
+    std::filesystem::path hdr = prefix;
+    hdr.replace_extension(".hdr");
+    std::ofstream out_hdr(hdr, std::ios::trunc);
+    if (!out_hdr) throw Error(errc::io_failure, "IoFailure: cannot open " + hdr.string() + " for writing");
+    out_hdr << "ENVI\n"
+            << "samples = " << map.samples << "\n"
+            << "lines = " << map.lines << "\n"
+            << "bands = 1\n"
+            << "header offset = 0\n"
+            << "file type = ENVI Standard\n"
+            << "data type = 4\n"
+            << "interleave = bsq\n"
+            << "byte order = 0\n";
+    std::filesystem::path rawp = prefix;
+    rawp.replace_extension(".raw");
+    std::ofstream out(rawp, std::ios::binary | std::ios::trunc);
+    if (!out) throw Error(errc::io_failure, "IoFailure: cannot open " + rawp.string() + " for writing");
+    const size_t n = map.scores.size();
+    std::vector<char> raw(n * 4);
+    if (n) {
+        detail::DeviceBuffer ds(n * sizeof(double)), dr(n * 4);
+        detail::cuda(cudaMemcpy(ds.p, map.scores.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        detail::check(hsad_encode_score_map(ds.p, 8, static_cast<int64_t>(n), dr.p, nullptr));
+        detail::cuda(cudaMemcpy(raw.data(), dr.p, raw.size(), cudaMemcpyDeviceToHost), "D2H");
+    }
+    out.write(raw.data(), static_cast<std::streamsize>(raw.size()));
+    if (!out) throw Error(errc::io_failure, "IoFailure: short write to " + rawp.string());
 }
 
 // ---- ENVI decode and evaluation (cube.hpp:70-72, eval.hpp:14-45) ---------------------

@@ -178,6 +178,22 @@ hsad_status hsad_dwest_pairs(const double* d_cdiff, const double* d_mdiff, int64
                              double eigen_fraction, double* d_scores, int8_t* d_counts,
                              int8_t* d_route, void* stream);
 
+/* dual_window_samples (detect.cpp:150-157): the inner-box and annulus sample sets of pixel
+ * (row, col) in the reference's scan order (gather_box / gather_annulus, detect.cpp:83-117,
+ * mirror_index reflection). d_inner: inner^2 x bands doubles, d_outer: (outer^2 - inner^2) x
+ * bands doubles, sample-major (= the column-major `dimension x count` SampleSet::vectors).
+ * Errors: the window's validation errors, ConfigMismatch "dual_window_samples requires a
+ * dual window". */
+hsad_status hsad_dual_window_samples(const void* d_cube, int32_t elem_bytes, int64_t lines,
+                                     int64_t samples, int32_t bands, int64_t row, int64_t col,
+                                     const hsad_window* window, double* d_inner, double* d_outer,
+                                     void* stream);
+
+/* The payload of save_score_map (detect.cpp:291-318): n scores (score_bytes 8|4) -> n
+ * little-endian fp32 values, the .raw file of a 1-band ENVI BSQ data type 4 map. */
+hsad_status hsad_encode_score_map(const void* d_scores, int32_t score_bytes, int64_t n, void* d_raw,
+                                  void* stream);
+
 /* Fused multi-detector over a row strip. The image is `lines` x `samples` x
  * `bands`; the buffer d_cube holds global rows [buf_row0, buf_row0 + buf_rows)
  * (row strip plus mirror halo; hsad_strip_rows() computes the range) and the

@@ -8,13 +8,13 @@ reference's detector API (`hsad`) and the row-strip multi-GPU driver
 from . import _abi
 from .hsad import (DetectOptions, DetectRequest, DwestConfig, HsadError, ScoreMap,
                    WaveletFilterPair, WindowConfig, daubechies_filters, detect, detect_multi, reduce_detect,
-                   dwest, dwest_pairs, dwrx, local_rx, mirror_index, pipeline_host, reduce_cube, row_quantum,
-                   strip_rows)
+                   dual_window_samples, dwest, dwest_pairs, dwrx, encode_score_map, local_rx, mirror_index, pipeline_host, reduce_cube, row_quantum,
+                   save_score_map, strip_rows)
 
 _abi.lib()  # no CPU fallback: fail at import when libhsad_b200.so is missing
 
 __all__ = [
     "DetectOptions", "DetectRequest", "DwestConfig", "HsadError", "ScoreMap", "WaveletFilterPair",
-    "WindowConfig", "daubechies_filters", "detect", "detect_multi", "reduce_detect", "dwest", "dwest_pairs", "dwrx", "local_rx",
-    "mirror_index", "pipeline_host", "reduce_cube", "row_quantum", "strip_rows",
+    "WindowConfig", "daubechies_filters", "detect", "detect_multi", "reduce_detect", "dual_window_samples", "dwest", "dwest_pairs", "dwrx", "encode_score_map", "local_rx",
+    "mirror_index", "pipeline_host", "reduce_cube", "row_quantum", "save_score_map", "strip_rows",
 ]

@@ -42,7 +42,8 @@ EXPORTED = [
     "hsad_read_cube", "hsad_reduce_raw", "hsad_pipeline_raw", "hsad_pipeline_sharded", "hsad_roc", "hsad_top_k", "hsad_adaptive_threshold", "hsad_render_pgm",
     "hsad_strip_plan", "hsad_gather_maps", "hsad_nccl_available", "hsad_nccl_unique_id",
     "hsad_nccl_comm_init_rank", "hsad_nccl_comm_init_all", "hsad_nccl_comm_destroy",
-    "hsad_last_reduce_detect_fused", "hsad_dwest_pairs",
+    "hsad_last_reduce_detect_fused", "hsad_dwest_pairs", "hsad_dual_window_samples",
+    "hsad_encode_score_map",
 ]
 
 HSAD_BSQ, HSAD_BIL, HSAD_BIP = 0, 1, 2
@@ -131,6 +132,8 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
         "hsad_nccl_comm_destroy": (I32, [VP]),
         "hsad_last_reduce_detect_fused": (I32, []),
         "hsad_dwest_pairs": (I32, [VP, VP, I64, D, VP, VP, VP, VP]),
+        "hsad_dual_window_samples": (I32, [VP, I32, I64, I64, I32, I64, I64, P(Window), VP, VP, VP]),
+        "hsad_encode_score_map": (I32, [VP, I32, I64, VP, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -342,6 +342,46 @@ def dwest_pairs(cdiff: torch.Tensor, mdiff: torch.Tensor, eigen_fraction: float 
     return scores, counts, route
 
 
+def dual_window_samples(cube: torch.Tensor, row: int, col: int, config: WindowConfig):
+    """hsad::dual_window_samples (detect.cpp:150-157): (inner, outer) sample sets of one pixel as
+    (count, bands) fp64 tensors in the reference's scan order (= SampleSet::vectors transposed)."""
+    cube = _require_cuda(cube, "cube")
+    lines, samples, bands = cube.shape
+    win = config.to_c()
+    n_in = max(config.inner_size, 0) ** 2
+    n_out = max(max(config.outer_size, 0) ** 2 - n_in, 0)
+    inner = torch.empty((n_in, bands), dtype=torch.float64, device=cube.device)
+    outer = torch.empty((n_out, bands), dtype=torch.float64, device=cube.device)
+    _check(_abi.lib().hsad_dual_window_samples(cube.data_ptr(), cube.element_size(), lines, samples, bands,
+                                               int(row), int(col), C.byref(win), inner.data_ptr(),
+                                               outer.data_ptr(), _stream_ptr()))
+    return inner, outer
+
+
+def encode_score_map(scores: torch.Tensor) -> torch.Tensor:
+    """The .raw payload of save_score_map (detect.cpp:291-318): little-endian fp32, as uint8."""
+    scores = _require_cuda(scores, "scores")
+    raw = torch.empty(scores.numel() * 4, dtype=torch.uint8, device=scores.device)
+    _check(_abi.lib().hsad_encode_score_map(scores.data_ptr(), scores.element_size(), scores.numel(),
+                                            raw.data_ptr(), _stream_ptr()))
+    return raw
+
+
+def save_score_map(score_map: "ScoreMap", prefix) -> None:
+    """hsad::save_score_map (detect.cpp:291-318): <prefix>.hdr (ENVI text, cube.cpp:184-196) and
+    <prefix>.raw (1 band, BSQ, data type 4, little-endian), the payload encoded on the device."""
+    from pathlib import Path
+    prefix = Path(prefix)
+    hdr = ("ENVI\n" f"samples = {score_map.samples}\n" f"lines = {score_map.lines}\n" "bands = 1\n"
+           "header offset = 0\n" "file type = ENVI Standard\n" "data type = 4\n"
+           "interleave = bsq\n" "byte order = 0\n")
+    try:
+        prefix.with_suffix(".hdr").write_text(hdr)
+        prefix.with_suffix(".raw").write_bytes(encode_score_map(score_map.scores).cpu().numpy().tobytes())
+    except OSError as e:
+        raise HsadError(_abi.HSAD_E_IO_FAILURE, f"IoFailure: cannot open {e.filename} for writing") from e
+
+
 def detect(cube: torch.Tensor, algorithm: str, config: WindowConfig,
            options: DetectOptions = DetectOptions()) -> ScoreMap:
     """hsad::detect dispatch (detect.cpp:278-289)."""

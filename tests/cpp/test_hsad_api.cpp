@@ -4,6 +4,9 @@
 // Built and run by tests/test_cpp_api.py (-m gpu). Exit code = failures.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <cstdlib>
 #include <string>
 
@@ -204,6 +207,50 @@ int main() {
         CHECK(std::abs(th.tau - (0.75 + std::sqrt(0.0125))) < 1e-12 && th.mask.mask[0] == 1 && th.mask.mask[1] == 0);
         auto pgm = render_pgm(m);
         CHECK(pgm.size() == 11 + 4 && pgm[11] == 255 && pgm[14] == 0 && pgm[12] == 170);
+    }
+    // dual_window_samples counts (proj/tests/test_detect.cpp:45-74)
+    {
+        auto cube = random_cube(20, 20, 3, 3);
+        auto [i513, o513] = dual_window_samples(cube, 10, 10, WindowConfig::dual(5, 13));
+        CHECK(i513.count() == 25 && o513.count() == 144);
+        auto [i313, o313] = dual_window_samples(cube, 10, 10, WindowConfig::dual(3, 13));
+        CHECK(i313.count() == 9 && o313.count() == 160);
+        auto [i13, o13] = dual_window_samples(cube, 10, 10, WindowConfig::dual(1, 3));
+        CHECK(i13.count() == 1 && o13.count() == 8);
+        bool same = true;
+        for (int b = 0; b < 3; ++b) same = same && i13.col(0)[b] == cube.at(10, 10, b);
+        int idx = 0;
+        for (int dr = -1; dr <= 1; ++dr)
+            for (int dc = -1; dc <= 1; ++dc) {
+                if (dr == 0 && dc == 0) continue;
+                for (int b = 0; b < 3; ++b) same = same && o13.col(idx)[b] == cube.at(10 + dr, 10 + dc, b);
+                ++idx;
+            }
+        CHECK(same);
+        // reflection at a corner: (0, 0) with a 3/5 window reads mirrored rows and columns
+        auto [ic, oc] = dual_window_samples(cube, 0, 0, WindowConfig::dual(3, 5));
+        CHECK(ic.count() == 9 && oc.count() == 16);
+        CHECK(ic.col(0)[1] == cube.at(1, 1, 1) && oc.col(0)[2] == cube.at(2, 2, 2));
+        CHECK_THROWS_CODE(dual_window_samples(cube, 0, 0, WindowConfig::single(5)), errc::config_mismatch);
+    }
+    // save_score_map (proj/tests/test_detect.cpp:250-262): fp32 little-endian payload + ENVI header
+    {
+        auto cube = random_cube(6, 7, 2, 11);
+        auto map = local_rx(cube, WindowConfig::single(3), 1e-6);
+        auto dir = std::filesystem::temp_directory_path() / "hsad_b200_scoremap_test";
+        std::filesystem::create_directories(dir);
+        save_score_map(map, dir / "scores");
+        std::ifstream hdr(dir / "scores.hdr");
+        std::string text((std::istreambuf_iterator<char>(hdr)), std::istreambuf_iterator<char>());
+        CHECK(text == "ENVI\nsamples = 7\nlines = 6\nbands = 1\nheader offset = 0\nfile type = ENVI Standard\n"
+                      "data type = 4\ninterleave = bsq\nbyte order = 0\n");
+        std::ifstream raw(dir / "scores.raw", std::ios::binary);
+        std::vector<float> back(map.scores.size());
+        raw.read(reinterpret_cast<char*>(back.data()), static_cast<std::streamsize>(back.size() * 4));
+        bool ok = raw.gcount() == static_cast<std::streamsize>(back.size() * 4);
+        for (size_t i = 0; i < back.size(); ++i) ok = ok && back[i] == static_cast<float>(map.scores[i]);
+        CHECK(ok);
+        std::filesystem::remove_all(dir);
     }
     std::printf("cpp drop-in: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
