@@ -357,7 +357,7 @@ def detector_ncu():
     """Issue-active and fp64-pipe utilisation of the four detector launches from the
     committed ncu --set full capture of this workload (the detectors' own roofline is
     fp64 issue, not HBM: ~57 B/px of DRAM traffic per launch)."""
-    f = ROOT / "profiles" / "ncu_full_r2_sweep.json"
+    f = ROOT / "profiles" / "ncu_full_r2b_sweep.json"
     if not f.exists():
         return {}
     d = json.loads(f.read_text())
@@ -383,7 +383,7 @@ def detector_ncu():
             "ncu_fp64_pipe_frac": [round(float(k[key_f]) / 100, 3) for k in det],
             "ncu_fp64_tflops_executed": [fp64_tflops(k) for k in det],
             "fp64_peak_tflops_measured": fp64_peak, "fp64_peak_source": peak_src,
-            "ncu_source": "profiles/ncu_full_r2_sweep.json (fast passes of the 7/3, 11/5, 15/5, 21/7 detectors)"}
+            "ncu_source": "profiles/ncu_full_r2b_sweep.json (fast passes of the 7/3, 11/5, 15/5, 21/7 detectors)"}
 
 
 def run_config(args, cfg, world):
@@ -588,7 +588,7 @@ def run_b200(args, cfg, rank, world, local, dist):
     step_gbs = value * 1e6 * bpp / 1e9
     # DRAM traffic per launch from the committed ncu --set full capture of this workload
     traffic, traffic_src = None, None
-    tfile = ROOT / "profiles" / "ncu_traffic_r2_sweep.json"
+    tfile = ROOT / "profiles" / "ncu_traffic_r2b_sweep.json"
     if args.config == "C5" and world == 1 and tfile.exists():
         tj = json.loads(tfile.read_text())
         traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in tj["launches"]) / 1e9

@@ -32,6 +32,8 @@ def label(i, name, seen):
     zero-window counting pass that follows each fast pass."""
     if "reduce" in name:
         return "reduce (K1)"
+    if "detect_kernel_flagged<" in name:  # the counting pass over the tiles the fast pass flagged
+        return f"detect {WINDOWS[(seen['fast'] - 1) % 4]} counting pass"
     args = name.split("detect_kernel<", 1)[1].split(">", 1)[0].replace("(bool)", "").replace("(int)", "")
     args = [a.strip() for a in args.split(",")]
     if len(args) >= 5 and args[4] in ("1", "true"):  # ZC: the zero-window counting pass
@@ -55,6 +57,8 @@ def main():
     for i, r in enumerate(rows[2:]):
         d = dict(zip(hdr, r))
         u = dict(zip(hdr, units))
+        if "hsad_b200" not in d["Kernel Name"]:  # torch fills of the probe script
+            continue
         ent = {"kernel": d["Kernel Name"], "launch": label(i, d["Kernel Name"], seen)}
         for m in METRICS:
             ent[m] = d.get(m)
