@@ -455,7 +455,20 @@ def run_b200(args, cfg, rank, world, local, dist):
     # HSAD_TORCH_GATHER=1 uses torch.distributed.gather instead
     gather = None
     if world > 1:
-        gather = MapGather(plan, dist) if os.environ.get("HSAD_TORCH_GATHER") else NcclMapGather(plan, dist)
+        if os.environ.get("HSAD_TORCH_GATHER"):
+            gather = MapGather(plan, dist)
+        else:
+            # every rank must take the same route: agree on whether the library's communicator came up
+            try:
+                gather, ok = NcclMapGather(plan, dist), 1
+            except Exception as e:  # e.g. no loadable libnccl.so.2 for the C-ABI on this box
+                print(f"[bench] hsad_gather_maps unavailable on rank {rank} ({e}); using torch.distributed.gather",
+                      file=sys.stderr, flush=True)
+                gather, ok = None, 0
+            flag = torch.tensor([ok], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                gather = MapGather(plan, dist)
     pad = lambda dt: torch.zeros((max(per, r1 - r0), samples), dtype=dt, device=dev)  # noqa: E731
     outs_pad = [(pad(torch.float64), pad(torch.int8) if r.eigcount else None) for r in reqs]
     outs = [(sc[: r1 - r0], None if cnt is None else cnt[: r1 - r0]) for sc, cnt in outs_pad]
