@@ -908,9 +908,11 @@ __device__ __noinline__ void dwest_jacobi4(const double (&A)[4][4], const double
 //      adj(T - lambda I) with the largest diagonal entry theta_k phi_{k+1} (leading and
 //      trailing principal minors), mapped back through the rotation and the reflector;
 //   5. sign rule, projection, count.
-// Pixels the two-pair route cannot settle — a third eigenvalue at or near the cutoff, a
-// selected eigenvalue closer than kDw4Gap (in units of |A|) to a neighbour, an iteration
-// that did not converge — take the general Jacobi route instead (a few 1e-4 of C5).
+// A third selected eigenvalue (lambda_3 from the remaining quadratic, polished the same
+// way) gets its own pass. Pixels the route cannot settle — an eigenvalue within 1e-6 of
+// the cutoff, four selected eigenvalues, a selected eigenvalue closer than kDw4Gap (in
+// units of |A|) to a neighbour, an iteration that did not converge — take the general
+// Jacobi route instead (a few 1e-4 of C5).
 constexpr double kDw4Gap = 3e-5;
 constexpr double kDw4LagTol = 1e-6;
 
@@ -1113,20 +1115,29 @@ __device__ __forceinline__ bool dwest4_fast(const double (&A)[4][4], const doubl
     }
     double lam2 = x;
     ok = tri4_polish(T, lam2) && ok;
-    //    lambda_3 from the remaining quadratic x^2 + r1 x + r0 (only its distance to the
-    //    cutoff and to lambda_2 matters)
+    //    lambda_3 >= lambda_4 from the remaining quadratic x^2 + r1 x + r0
     const double r1 = q2 + lam2, r0 = fma(lam2, r1, q1);
-    const double lam3 = 0.5 * (sqrt_pos(fmax(fma(r1, r1, -4.0 * r0), 0.0)) - r1);
+    double lam3 = 0.5 * (sqrt_pos(fmax(fma(r1, r1, -4.0 * r0), 0.0)) - r1);
     const double cut = __dmul_rn(frac, lam1);
+    const double margin = fma(1e-6, cut, 1e-9);  // an eigenvalue this close to the cutoff: general route
     const bool take2 = lam2 > 0.0 && !(lam2 < cut);
-    // the two-pair route settles the pixel when lambda_3 is clearly below the cutoff and
-    // every selected eigenvalue is clear of its neighbours
-    ok = ok && lam3 < cut - fma(1e-6, cut, 1e-9) && lam1 - lam2 >= kDw4Gap && (!take2 || lam2 - lam3 >= kDw4Gap);
-    // 4./5. eigenvectors, sign rule, projection
-    double proj = tri4_project(T, lam1, md);
-    if (take2) proj += tri4_project(T, lam2, md);
+    bool take3 = false;
+    if (take2 && lam3 > cut + margin) {  // a third selected eigenvalue (0.03% of the C5 pixels)
+        take3 = true;
+        const double lam4 = -r1 - lam3;  // before the polish: the quadratic's own pair
+        ok = tri4_polish(T, lam3) && ok && lam4 < cut - margin && lam3 - lam4 >= kDw4Gap;
+    } else {
+        ok = ok && lam3 < cut - margin;
+    }
+    // the route settles the pixel when no eigenvalue sits at the cutoff and every selected
+    // eigenvalue is clear of its neighbours
+    ok = ok && lam1 - lam2 >= kDw4Gap && (!take2 || lam2 - lam3 >= kDw4Gap);
+    // 4./5. eigenvectors, sign rule, projection: one pass per selected eigenvalue
+    count = take3 ? 3 : take2 ? 2 : 1;
+    double proj = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < count; ++k) proj += tri4_project(T, k == 0 ? lam1 : k == 1 ? lam2 : lam3, md);
     score = fabs(proj);
-    count = take2 ? 2 : 1;
     return ok;
 }
 

@@ -3,7 +3,7 @@ end-to-end time through hsad_pipeline_host (pinned host cube in, host maps out),
 oracle on all host cores for the same job, and the parity gates (max rel diff vs the oracle,
 identical DWEST eigen-counts, identical top-k sets with k = truth positives).
 
-    python scripts/probe_configs.py > profiles/configs_r1.json
+    python scripts/probe_configs.py > profiles/configs_r2.json
 """
 import json
 import os
