@@ -164,3 +164,21 @@ def test_third_eigenvalue_near_cutoff_takes_general_route():
     s, c, r = _run(A, m, 0.1)
     assert (r == 1).all()
     assert (c[: n // 2] == 3).all() and (c[n // 2:] == 2).all()
+
+
+def test_three_selected_eigenvalues_stay_on_the_tridiagonal_route():
+    rng = np.random.default_rng(13)
+    n = 50_000
+    lam = np.stack([rng.uniform(0.8, 1.2, n), rng.uniform(0.4, 0.6, n), rng.uniform(0.15, 0.3, n),
+                    -rng.uniform(0.1, 2.0, n)], 1)
+    A = _sym(rng, n, lam)
+    m = rng.standard_normal((n, 4))
+    r = _check(A, m, 0.1, "three selected", min_fast=0.99)
+    s, c, _ = _run(0.5 * (A + A.transpose(0, 2, 1)), m, 0.1)
+    assert (c == 3).all()
+    # four selected: the general route
+    lam[:, 3] = rng.uniform(0.125, 0.145, n)  # above every cutoff (<= 0.12)
+    B = _sym(rng, n, lam)
+    s, c, r = _run(0.5 * (B + B.transpose(0, 2, 1)), m, 0.1)
+    assert (c == 4).all() and (r == 1).all()
+    _check(B, m, 0.1, "four selected")
