@@ -895,8 +895,8 @@ __device__ __noinline__ void dwest_jacobi4(const double (&A)[4][4], const double
 // ---- DWEST for 4 bands without a full eigendecomposition -----------------------------
 // Only the eigenpairs with lambda >= f lambda_max > 0 enter the score (one for ~83% of
 // the C5 pixels, two for ~16%, three for 0.03%), so the 4 x 4 problem is solved for the
-// top two pairs only, each to fp64 backward-stable accuracy (eps |A| / gap, like the
-// reference's QL iteration):
+// selected pairs only (up to three), each to fp64 backward-stable accuracy (eps |A| / gap,
+// like the reference's QL iteration):
 //   1. scale by a power of two (exact) so max |a_ij| is in [1, 2);
 //   2. tridiagonalise: one Householder reflector (column 0) + one plane rotation;
 //   3. monic characteristic polynomial of the tridiagonal T; lambda_1 by Laguerre's
