@@ -1146,10 +1146,28 @@ template <int L>
 __device__ __forceinline__ void dwest_score(const double (&A)[L][L], const double (&md)[L], double frac,
                                             double& score, int& count) {
     if constexpr (L == 4) {
+        double s1 = 0.0;
+        int c1 = 0;
 #ifndef HSAD_DWEST_JACOBI
-        if (!dwest4_fast(A, md, frac, score, count))
+        if (!dwest4_fast(A, md, frac, s1, c1))
 #endif
-            dwest_jacobi4(A, md, frac, score, count);
+        {
+            // the out-of-line route takes its arguments in local memory: copy them here, in the
+            // rare branch, so the common path keeps the statistics in registers
+            double Ac[4][4], mc[4], s2;
+            int c2;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                mc[i] = md[i];
+#pragma unroll
+                for (int j = i; j < 4; ++j) Ac[i][j] = A[i][j];
+            }
+            dwest_jacobi4(Ac, mc, frac, s2, c2);
+            s1 = s2;
+            c1 = c2;
+        }
+        score = s1;
+        count = c1;
     } else {
         dwest_jacobi_body<L>(A, md, frac, score, count);
     }
@@ -1644,10 +1662,16 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
                     // entering rows finds every zero spectrum
                     if constexpr (ZC) s_nz[k * ncol + c] += nz_in - nz_out;
                     else if (k == 0 && !nz_in) s_zero_seen = 1;
+                    // m(yin) - m(yout), rounded as add_moments(+yin) then add_moments(-yout) onto 0
+                    {
+                        int cc = L;
 #pragma unroll
-                    for (int i = 0; i < NC; ++i) dm[i] = 0.0;
-                    add_moments<L>(dm, yin, 1.0);
-                    add_moments<L>(dm, yout, -1.0);
+                        for (int i = 0; i < L; ++i) dm[i] = yin[i] - yout[i];
+#pragma unroll
+                        for (int i = 0; i < L; ++i)
+#pragma unroll
+                            for (int j = i; j < L; ++j) dm[cc++] = fma(-yout[i], yout[j], __dmul_rn(yin[i], yin[j]));
+                    }
                     double2* dst = vslot(k, c);
 #pragma unroll
                     for (int c2 = 0; c2 < NC2; ++c2) {
@@ -1692,9 +1716,16 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
                     const bool odd = (t & 1) != 0;
                     const int own = P.rmax + seg0;
                     double h[NC];
+                    {  // d = 0 (R >= kPairRadius >= 1): the lane's own column starts the sum
+                        const double2* src = vslot(k, own);
 #pragma unroll
-                    for (int i = 0; i < NC; ++i) h[i] = 0.0;
-                    for (int d = 0; d < R; ++d) {
+                        for (int c2 = 0; c2 < NC2; ++c2) {
+                            const double2 v = src[c2];
+                            h[2 * c2] = v.x;
+                            if (2 * c2 + 1 < NC) h[2 * c2 + 1] = v.y;
+                        }
+                    }
+                    for (int d = 1; d < R; ++d) {
                         const double2* src = vslot(k, odd ? own + d : own - d);
 #pragma unroll
                         for (int c2 = 0; c2 < NC2; ++c2) {
