@@ -100,6 +100,8 @@ struct DetectParams {
     const double* wmap;    // ... and the composed wavelet map (4 x raw_bands)
     int trio;        // std layout with exactly one LRX, one DWRX and one DWEST request ...
     int trio_q[3];   // ... at these request positions (solve_trio interleaves their solves)
+    ReqDev treq[3];  // ... and their copies in LRX, DWRX, DWEST order: compile-time indices, so the
+                     // solver reads ridge / fraction / map pointers straight from the constant bank
     int staged;      // STD kernel: the update rows arrive in shared memory by TMA bulk copies
     unsigned char* zflag;  // per-CTA "saw an all-zero spectrum" (fast pass -> counting pass)
     int has_dual;
@@ -774,7 +776,7 @@ __device__ __forceinline__ void lrx_solve(const DetectParams& P, int q, const Re
             if constexpr (ZC) code = repair_pixel<L>(P, R, r, col, score);
             else s_zero_seen = 1, code = 0;  // the counting pass recomputes this CTA
         }
-        if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
+        if (P.diag_lin >= 0 && lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
             report(P, q, r, col, code);
             score = 0.0;
@@ -831,7 +833,7 @@ __device__ __forceinline__ void dwrx_solve(const DetectParams& P, int q, const R
             if constexpr (ZC) code = repair_pixel<L>(P, R, r, col, score);
             else s_zero_seen = 1, code = 0;  // the counting pass recomputes this CTA
         }
-        if (lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
+        if (P.diag_lin >= 0 && lin == P.diag_lin && P.req_base + q == P.diag_req) *P.diag_out = delta;
         if (code) {
             report(P, q, r, col, code);
             score = 0.0;
@@ -1242,10 +1244,10 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
                                            int cnt0, int cnt1, int nzc, const double (&yc)[L], int64_t r,
                                            int64_t col, int64_t o, int64_t lin) {
     constexpr int NC = Dim<L>::NC;
-    const int qL = P.trio_q[0], qR = P.trio_q[1], qE = P.trio_q[2];
-    const ReqDev& RL = s_req[qL];
-    const ReqDev& RR = s_req[qR];
-    const ReqDev& RE = s_req[qE];
+    const int qL = P.trio_q[0], qR = P.trio_q[1];
+    const ReqDev& RL = P.treq[0];
+    const ReqDev& RR = P.treq[1];
+    const ReqDev& RE = P.treq[2];
     double bg[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) bg[c] = S0[c];
@@ -1277,7 +1279,6 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
     } else {
         double score = 0.0;
         if (dnzL) {
-            if (lin == P.diag_lin && P.req_base + qL == P.diag_req) *P.diag_out = deltaL;
             score = scoreL;
             if (codeL == kIllConditioned) {
                 if constexpr (ZC) codeL = repair_pixel<L>(P, RL, r, col, score);
@@ -1294,7 +1295,6 @@ __device__ __forceinline__ void solve_trio(const DetectParams& P, const ReqDev* 
     {
         double score = 0.0;
         if (D.mnz) {
-            if (lin == P.diag_lin && P.req_base + qR == P.diag_req) *P.diag_out = deltaR;
             score = scoreR;
             if (codeR == kIllConditioned) {
                 if constexpr (ZC) codeR = repair_pixel<L>(P, RR, r, col, score);
@@ -1607,13 +1607,38 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
     PT_START();
     const bool owner1 = K == 1 && seg0 < P.tw && c0 + seg0 < P.samples;
     const char* own_cb = colbase_of(P.rmax + seg0);
+    // stage column of strip column c: every column a valid output's window reads mirrors
+    // into [lo, hi); the clamp only guards the unused tail columns of a strip that runs past
+    // the image. Row-invariant: the thread's first column's is kept across the row loop.
+    auto scol_of = [&](int c) {
+        return min(max(mirror32(static_cast<int>(c0 - P.rmax + c), static_cast<int>(P.samples)) -
+                           static_cast<int>(st_lo),
+                       0),
+                   static_cast<int>(st_hi - st_lo) - 1);
+    };
+    const int scol_t = scol_of(t);
+    // K = 1 on an fp64 cube: the centre spectrum of row r through a running pointer (the row is
+    // inside the image and the buffer: no reflection)
+    const double* own_p = reinterpret_cast<const double*>(own_cb + (ra - P.buf_row0) * row_bytes);
     for (int64_t r = ra; r < rb; ++r) {
         // K = 1: fetch the centre spectrum first; its latency hides behind the
         // vertical update, the barrier and the horizontal sums
         // (raw values: the shift and the zero test wait until the spectrum is used, so
         // the load is in flight across the update and the barrier)
         double yc1[L];
-        if (owner1) load_row<L, STD, FUSE>(P, own_cb, row_bytes, static_cast<int>(r), yc1);
+        if constexpr (STD && !FUSE && L % 2 == 0) {
+            if (owner1) {
+#pragma unroll
+                for (int i = 0; i < L; i += 2) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(own_p + i));
+                    yc1[i] = v.x;
+                    yc1[i + 1] = v.y;
+                }
+            }
+            own_p += P.samples * L;
+        } else {
+            if (owner1) load_row<L, STD, FUSE>(P, own_cb, row_bytes, static_cast<int>(r), yc1);
+        }
         if (r > ra) {
             if constexpr (STD) {
                 mbar_wait(&s_bar, st_phase);
@@ -1621,14 +1646,7 @@ __device__ __forceinline__ void detect_tile(const DetectParams& P, int bx, int b
             }
             for (int c = t; c < ncol; c += NT) {
                 const char* cb = colbase_of(c);
-                // stage column of strip column c: every column a valid output's window
-                // reads mirrors into [lo, hi); the clamp only guards the unused tail
-                // columns of a strip that runs past the image
-                const int scol = min(max(mirror32(static_cast<int>(c0 - P.rmax + c),
-                                                  static_cast<int>(P.samples)) -
-                                             static_cast<int>(st_lo),
-                                         0),
-                                     static_cast<int>(st_hi - st_lo) - 1);
+                const int scol = c == t ? scol_t : scol_of(c);
 #pragma unroll
                 for (int k = 0; k < NBOX; ++k) {
                     const int R = P.radius[k];
@@ -2065,7 +2083,10 @@ hsad_status plan_requests(const hsad_detect_request* reqs, int n, Plan& plan) {
         for (int q = 0; q < n; ++q) seen[P.req[q].algo] = q;
         if (seen[0] >= 0 && seen[1] >= 0 && seen[2] >= 0 && !getenv("HSAD_NO_TRIO")) {
             P.trio = 1;
-            for (int a = 0; a < 3; ++a) P.trio_q[a] = seen[a];
+            for (int a = 0; a < 3; ++a) {
+                P.trio_q[a] = seen[a];
+                P.treq[a] = P.req[seen[a]];
+            }
         }
     }
     P.rmax = 0;
@@ -2329,6 +2350,7 @@ hsad_status detect_group_impl(const void* d_cube, int32_t elem_bytes, int64_t li
             D.diag_lin = lin;
             D.diag_req = fail_req;
             D.diag_out = d_diag;
+            D.trio = 0;  // the per-request solves report the ridge (same arithmetic; the trio kernel carries no diagnostics)
             // the diagnostic pass writes into scratch rows, never over the results
             char* scratch = nullptr;
             e = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_stride * D.nreq, s);
