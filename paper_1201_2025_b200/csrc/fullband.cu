@@ -416,6 +416,29 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    if (P.gram) {
+        // tensor-core route: G = sum_k (x_k - s)(x_k - s)^T came from tc_gram_kernel (exact
+        // integer accumulation, one rounding); C = G / N - (mu - s)(mu - s)^T
+        if (own) {
+            const double2* g2 = reinterpret_cast<const double2*>(
+                P.gram + (((r - P.gram_row0) * P.samples + c) * ntiles + t) * 64);
+            const double invN = 1.0 / N;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                const int i = 8 * ti + a;
+                const double yi = i < L ? mu[i] - P.shift[i] : 0.0;
+#pragma unroll
+                for (int b = 0; b < 8; b += 2) {
+                    const double2 g = __ldg(g2 + a * 4 + b / 2);
+                    const int k = 8 * tk + b;
+                    const double y0 = k < L ? mu[k] - P.shift[k] : 0.0;
+                    const double y1 = k + 1 < L ? mu[k + 1] - P.shift[k + 1] : 0.0;
+                    acc[a][b] = (i < L && k < L) ? fma(-yi, y0, g.x * invN) : 0.0;
+                    acc[a][b + 1] = (i < L && k + 1 < L) ? fma(-yi, y1, g.y * invN) : 0.0;
+                }
+            }
+        }
+    } else {
 #ifdef HSAD_FB_SYNC_CHUNKS
     for (int k0 = 0; k0 < N; k0 += CH) {
         const int nk = min(CH, N - k0);
@@ -523,6 +546,7 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 8; ++b) acc[a][b] *= invN;
+    }  // !P.gram
     if (own && ti == tk)
 #pragma unroll
         for (int a = 0; a < 8; ++a) dg[8 * ti + a] = acc[a][a];
@@ -701,6 +725,29 @@ extern "C" void hsad_fb_phase_cycles(unsigned long long* out, int reset) {
 }
 #endif
 
+bool fullband_tc_applies(const FbParams& P);                                  // fullband_tc.cu
+hsad_status fullband_tc_launch(FbParams& P, cudaStream_t s, double* gram_out, double* shift_unit_out);
+
+// The register-tile kernel over rows [row_begin, row_end) (bands + 1 <= 192).
+hsad_status fullband_reg_launch(FbParams& P, cudaStream_t s) {
+    const int64_t rows = P.row_end - P.row_begin;
+    if (rows > 65535) return set_error(HSAD_E_UNSUPPORTED, "strip too tall for one launch");
+    dim3 grid(static_cast<unsigned>(P.samples), static_cast<unsigned>(rows));
+    const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;  // >= N + inner^2
+    P.mp = ((P.bands + 1) + 7) / 8 * 8;
+    P.chunk = 32;
+    const size_t smem = (static_cast<size_t>(P.chunk) * (P.mp / 8) * 10 + 3 * P.mp +
+                         2 * (8 * (P.mp / 8) * 10 + 8) + nsamp) * 8 +
+                        2 * static_cast<size_t>(P.chunk) * P.bands * P.elem_bytes;  // cp.async stage
+    HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    const int T = P.mp / 8;
+    const int nt = (T * (T + 1) / 2 + 31) / 32 * 32;
+    fullband_reg_kernel<<<grid, nt, smem, s>>>(P);
+    HSAD_CUDA_TRY(cudaGetLastError());
+    return HSAD_OK;
+}
+
 // Shared memory and launch shape for one full-band request.
 hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
     if (P.bands > kFbMaxBands)
@@ -712,20 +759,11 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
     const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;  // >= N + inner^2
     const int mp8 = ((P.bands + 1) + 7) / 8 * 8;
     if (mp8 <= kFbRegMaxMp && !getenv("HSAD_FB_PACKED")) {
-        // register-resident tiles: shared memory holds only samples and vectors
-        P.mp = mp8;
-        P.chunk = 32;
-        const size_t smem = (static_cast<size_t>(P.chunk) * (P.mp / 8) * 10 + 3 * P.mp +
-                             2 * (8 * (P.mp / 8) * 10 + 8) + nsamp) * 8 +
-                            2 * static_cast<size_t>(P.chunk) * P.bands * P.elem_bytes;  // cp.async stage
-        HSAD_CUDA_TRY(cudaFuncSetAttribute(fullband_reg_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem)));
-        const int T = P.mp / 8;
-        const int nt = (T * (T + 1) / 2 + 31) / 32 * 32;
-        fullband_reg_kernel<<<grid, nt, smem, s>>>(P);
-        HSAD_CUDA_TRY(cudaGetLastError());
-        return HSAD_OK;
+        // register-resident tiles: shared memory holds only samples and vectors; the Gram
+        // comes from the tensor cores unless HSAD_FB_TC=0
+        P.gram = nullptr;
+        if (fullband_tc_applies(P)) return fullband_tc_launch(P, s, nullptr, nullptr);
+        return fullband_reg_launch(P, s);
     }
     P.mp = ((P.bands + 1) + 3) / 4 * 4;
     const int64_t tri = static_cast<int64_t>(P.mp) * (P.mp + 1) / 2;

@@ -129,6 +129,11 @@ struct FbParams {
     int8_t* eigcount;   // DWEST eigen-count map (nullable)
     int chunk;          // samples per shared-memory chunk (set by fullband_launch)
     int mp;             // bordered dimension L+1 rounded up to a multiple of 4
+    // tensor-core route (fullband_tc.cu): the raw window Gram of the shifted samples,
+    // [row - gram_row0][col][8x8 tile][8][8], and the per-band shift; null = fp64 FMA Gram
+    const double* gram;
+    int64_t gram_row0;
+    const double* shift;
 };
 
 // Packed per-pixel failure word (atomicMin across a call): the request's position in
