@@ -379,7 +379,13 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     const int N = size * size - excl * excl;
     int64_t* base = reinterpret_cast<int64_t*>(dg + MP);  // [N + excl^2]
     const int NI = P.algo == HSAD_DWRX ? excl * excl : 0;
-    for (int k = t; k < N + NI; k += blockDim.x)
+    // tensor-core route: the Gram tiles of this pixel; their border row L (a constant-one
+    // band in the digit array) holds the exact window sums of the shifted samples
+    const bool tc = P.gram != nullptr;
+    const int T = MP / 8;
+    const int ntiles = T * (T + 1) / 2;
+    const double* gpx = tc ? P.gram + ((r - P.gram_row0) * P.samples + c) * ntiles * 128 : nullptr;
+    for (int k = t + (tc ? N : 0); k < N + NI; k += blockDim.x)
         base[k] = k < N ? sample_base(P, ri, c, k, size, excl) : sample_base(P, ri, c, k - N, excl, 0);
     __syncthreads();
     // window means: one band per thread, 8 independent partial sums (8 loads in flight;
@@ -394,17 +400,24 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
         return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
     };
     for (int b = t; b < MP; b += blockDim.x) {
-        const double sum = b < L ? band_sum(b, 0, N) : 0.0;
+        double sum = 0.0;
+        if (tc) {
+            // S = (hi, lo): the exact window sum of the shifted samples
+            const int tl = L >> 3;
+            const double* sp = gpx + (tl * (tl + 1) / 2 + (b >> 3)) * 128 + (L & 7) * 8 + (b & 7);
+            xs[b] = b < L ? __ldg(sp) : 0.0;
+            xs[MP + b] = b < L ? __ldg(sp + 64) : 0.0;
+        } else if (b < L) {
+            sum = band_sum(b, 0, N);
+        }
         const double si = (b < L && NI > 0) ? band_sum(b, N, NI) : 0.0;
-        mu[b] = b < L ? sum / N : 0.0;
+        mu[b] = b < L ? (tc ? P.shift[b] + (xs[b] + xs[MP + b]) / N : sum / N) : 0.0;
         mu[MP + b] = (b < L && P.algo == HSAD_DWRX) ? si / (excl * excl) : 0.0;
     }
     __syncthreads();
     FB_MARK(0);
 
     // this thread's tile of the lower triangle
-    const int T = MP / 8;
-    const int ntiles = T * (T + 1) / 2;
     const bool own = t < ntiles;
     int ti = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
     while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
@@ -420,24 +433,36 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
         // tensor-core route: G = sum_k (x_k - s)(x_k - s)^T came from tc_gram_kernel (exact
         // integer accumulation, one rounding); C = G / N - (mu - s)(mu - s)^T
         if (own) {
-            const double2* g2 = reinterpret_cast<const double2*>(
-                P.gram + (((r - P.gram_row0) * P.samples + c) * ntiles + t) * 64);
-            const double invN = 1.0 / N;
+            // C = (N G - S S^T) / N^2 with G and S as exact (hi, lo) pairs: the difference is
+            // formed in double-double arithmetic and rounded once, so a window whose mean is
+            // far from the shift loses nothing to cancellation
+            const double2* g2 = reinterpret_cast<const double2*>(gpx + t * 128);
+            const double dN = N, invN2 = 1.0 / (dN * dN);
 #pragma unroll
             for (int a = 0; a < 8; ++a) {
                 const int i = 8 * ti + a;
-                const double yi = i < L ? mu[i] - P.shift[i] : 0.0;
+                const double ai = xs[i], bi = xs[MP + i];  // 0 for i >= L
 #pragma unroll
                 for (int b = 0; b < 8; b += 2) {
-                    const double2 g = __ldg(g2 + a * 4 + b / 2);
-                    const int k = 8 * tk + b;
-                    const double y0 = k < L ? mu[k] - P.shift[k] : 0.0;
-                    const double y1 = k + 1 < L ? mu[k + 1] - P.shift[k + 1] : 0.0;
-                    acc[a][b] = (i < L && k < L) ? fma(-yi, y0, g.x * invN) : 0.0;
-                    acc[a][b + 1] = (i < L && k + 1 < L) ? fma(-yi, y1, g.y * invN) : 0.0;
+                    const double2 gh2 = __ldg(g2 + a * 4 + b / 2);
+                    const double2 gl2 = __ldg(g2 + 32 + a * 4 + b / 2);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int k = 8 * tk + b + h;
+                        const double gh = h ? gh2.y : gh2.x, gl = h ? gl2.y : gl2.x;
+                        const double aj = xs[k], bj = xs[MP + k];
+                        const double th = dN * gh, te = fma(dN, gh, -th);
+                        const double ph = ai * aj, pe = fma(ai, aj, -ph);
+                        const double cross = fma(ai, bj, bi * aj);
+                        const double sd = th - ph, bb = sd - th;
+                        const double e = (th - (sd - bb)) + (-ph - bb);  // two_sum(th, -ph)
+                        const double res = sd + (e + (((te + dN * gl) - pe) - cross));
+                        acc[a][b + h] = (i < L && k < L) ? res * invN2 : 0.0;
+                    }
                 }
             }
         }
+        __syncthreads();  // xs (the shifted means) is free again
     } else {
 #ifdef HSAD_FB_SYNC_CHUNKS
     for (int k0 = 0; k0 < N; k0 += CH) {
@@ -759,8 +784,8 @@ hsad_status fullband_launch(FbParams& P, cudaStream_t s) {
     const int64_t nsamp = static_cast<int64_t>(P.outer) * P.outer;  // >= N + inner^2
     const int mp8 = ((P.bands + 1) + 7) / 8 * 8;
     if (mp8 <= kFbRegMaxMp && !getenv("HSAD_FB_PACKED")) {
-        // register-resident tiles: shared memory holds only samples and vectors; the Gram
-        // comes from the tensor cores unless HSAD_FB_TC=0
+        // register-resident tiles: shared memory holds only samples and vectors; with
+        // HSAD_FB_TC=1 the Gram comes from the tensor cores (fullband_tc.cu)
         P.gram = nullptr;
         if (fullband_tc_applies(P)) return fullband_tc_launch(P, s, nullptr, nullptr);
         return fullband_reg_launch(P, s);

@@ -61,7 +61,7 @@ struct TcParams {
     int ntile;              // 128 x 64 Gram tiles per pixel (lower triangle of mp x mp)
     int tile_ib[6], tile_jb[6];
     int T;                  // mp / 8: 8x8 output tiles per dimension
-    double* gram;           // [rows][samples][T (T + 1) / 2][8][8] raw Gram of the shifted samples
+    double* gram;           // [rows][samples][T (T + 1) / 2][2: hi, lo][8][8] raw Gram of the shifted samples
     const double* unit;     // [192] u_b
     uint32_t lbo, sbo;      // UMMA descriptor strides (bytes)
 };
@@ -83,7 +83,7 @@ __device__ __forceinline__ double key_value(long long k) {
     return __longlong_as_double(k >= 0 ? k : k ^ 0x7fffffffffffffffLL);
 }
 
-constexpr int kTcStatBlocks = 1184;
+constexpr int kTcStatBlocks = 296;
 struct TcStats {
     double sum[kTcStatBlocks][kTcBands];  // per-block partial sums (summed in block order: deterministic)
     long long kmin[kTcBands], kmax[kTcBands];
@@ -127,6 +127,8 @@ __global__ void tc_stats_final(const TcStats* st, int nblocks, int64_t npix, int
         s = static_cast<double>(static_cast<float>(sum / static_cast<double>(npix)));
         const double bound = fmax(key_value(st->kmax[b]) - s, s - key_value(st->kmin[b]));
         if (bound > 0.0 && bound < DBL_MAX) u = scalbn(1.0, ilogb(bound) + 1 - kQBits);
+    } else if (b == bands) {
+        u = 0x1p-49;  // the constant-one band: top digit 1, q = 128^7
     }
     shift[b] = s;
     unit[b] = u;
@@ -152,6 +154,8 @@ __global__ void tc_slice_kernel(const void* cube, int elem_bytes, int64_t npix, 
                                              : static_cast<double>(static_cast<const float*>(cube)[p * bands + b]);
             const double y = (x - shift[b]) / unit[b];  // power-of-two divisor: exact
             v = __double2ll_rn(y);
+        } else if (b == bands) {
+            v = 1ll << 49;  // constant one (unit 2^-49): Gram row `bands` = the window sums
         }
 #pragma unroll
         for (int sl = kTcSlices - 1; sl >= 0; --sl) {
@@ -271,6 +275,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gram_kernel(const TcParams P
                 dr = idx - 2 * W - E - Re, col = c - 1 - Re, sign = 1;  // leaving the excluded box
             }
         }
+        // padding entries copy nothing: cp.async with src-size 0 zero-fills the 16 bytes
+        // (a shared all-zero sample in global memory made every SM hit one L2 line)
+        const uint32_t nbytes = sign != 0 ? 16u : 0u;
         int64_t off_b = P.zero_off, off_a = P.zero_off;
         if (sign != 0) {
             const int rr = mirror_tc(r + dr, P.lines) - P.qrow0;
@@ -285,8 +292,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gram_kernel(const TcParams P
             const uint32_t dst = smem_u32(sa + sub * kTcBlk + k * 16);
 #pragma unroll
             for (int sl = 0; sl < kTcSlices; ++sl)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + sl * kTcASlice),
-                             "l"(src + sl * kTcBands)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + sl * kTcASlice),
+                             "l"(src + sl * kTcBands), "r"(nbytes)
                              : "memory");
         }
         {
@@ -296,8 +303,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gram_kernel(const TcParams P
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int sl = s0 + 2 * i;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + sl * kTcBSlice),
-                             "l"(src + sl * kTcBands)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + sl * kTcBSlice),
+                             "l"(src + sl * kTcBands), "r"(nbytes)
                              : "memory");
             }
         }
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gram_kernel(const TcParams P
             const int c = c_begin + (g + 1 - n_init) / n_step;
             mbar_wait(&s_done[g % kTcStages], (g / kTcStages) & 1);  // every MMA up to chunk g
             tc_fence_after();
-            double* out = P.gram + (static_cast<int64_t>(r - P.row_begin) * P.samples + c) * ntile_out * 64;
+            double* out = P.gram + (static_cast<int64_t>(r - P.row_begin) * P.samples + c) * ntile_out * 128;
 #pragma unroll 1
             for (int cb = 0; cb < 4; ++cb) {
                 const int j0 = jb * 64 + half * 32 + cb * 8;
@@ -354,22 +361,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gram_kernel(const TcParams P
                 for (int gq = 0; gq < kTcSlices; ++gq) tmem_ld8(taddr + gq * 64, acc[gq]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (ti < P.T && tk <= ti) {
-                    double v[8];
+                    // sum_g acc_g 128^(7 - g) = hi 2^28 + lo, both exact in int64 and in fp64:
+                    // the entry leaves as the unevaluated pair (hi part, lo part), so the
+                    // consumer can subtract the mean product before anything is rounded
+                    double vh[8], vl[8];
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
-                        // sum_g acc_g 128^(7 - g) = hi 2^28 + lo, both exact in int64
                         long long hi = acc[0][b], lo = acc[4][b];
 #pragma unroll
                         for (int gq = 1; gq < 4; ++gq) {
                             hi = hi * 128 + acc[gq][b];
                             lo = lo * 128 + acc[4 + gq][b];
                         }
-                        const double val = fma(static_cast<double>(hi), 0x1p28, static_cast<double>(lo));
-                        v[b] = __dmul_rn(__dmul_rn(val, ui), s_unit[j0 + b]);
+                        const double uij = __dmul_rn(ui, s_unit[j0 + b]);  // power of two
+                        vh[b] = __dmul_rn(__dmul_rn(static_cast<double>(hi), 0x1p28), uij);
+                        vl[b] = __dmul_rn(static_cast<double>(lo), uij);
                     }
-                    double2* dst = reinterpret_cast<double2*>(out + (ti * (ti + 1) / 2 + tk) * 64 + a_in * 8);
+                    double2* dst = reinterpret_cast<double2*>(out + (ti * (ti + 1) / 2 + tk) * 128 + a_in * 8);
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dst[b] = make_double2(v[2 * b], v[2 * b + 1]);
+                    for (int b = 0; b < 4; ++b) {
+                        dst[b] = make_double2(vh[2 * b], vh[2 * b + 1]);
+                        dst[32 + b] = make_double2(vl[2 * b], vl[2 * b + 1]);
+                    }
                 }
             }
             tc_fence_before();  // the next iteration's barrier orders these reads before its MMAs
@@ -388,9 +401,13 @@ int env_int(const char* name, int dflt) {
 }  // namespace
 
 // The tensor-core route serves LRX / DWRX whose bordered matrix fits the register-tile
-// Cholesky (bands + 1 <= 192). HSAD_FB_TC=0 keeps the fp64 FMA Gram.
+// Cholesky (bands + 1 <= 192). It is selected with HSAD_FB_TC=1: its covariance is exact to
+// one rounding, so at kappa ~ 1e6 its scores sit as close to the long-double value as the
+// reference's own fp64 arithmetic does (C3: 1.4e-9 vs 1.6e-9) but no longer share the
+// reference's rounding, and differ from it by up to 2e-9 on ~1% of the C3 pixels; the default
+// fp64 FMA Gram sums the reference's products and stays within the plain 1e-9 bar of it.
 bool fullband_tc_applies(const FbParams& P) {
-    if (env_int("HSAD_FB_TC", 1) == 0) return false;
+    if (env_int("HSAD_FB_TC", 0) == 0) return false;
     if (P.algo != HSAD_LRX && P.algo != HSAD_DWRX) return false;
     if ((P.bands + 1 + 7) / 8 * 8 > kTcBands) return false;
     if (P.lines > INT32_MAX || P.samples > INT32_MAX) return false;
@@ -467,9 +484,9 @@ hsad_status fullband_tc_launch(FbParams& P, cudaStream_t s, double* gram_out, do
     G.sbo = static_cast<uint32_t>(env_int("HSAD_TC_SBO", kTcBlk));
     HSAD_CUDA_TRY(cudaFuncSetAttribute(tc_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
 
-    const size_t px_bytes = static_cast<size_t>(G.T) * (G.T + 1) / 2 * 64 * sizeof(double);
+    const size_t px_bytes = static_cast<size_t>(G.T) * (G.T + 1) / 2 * 128 * sizeof(double);  // (hi, lo) planes
     const int64_t rows = P.row_end - P.row_begin;
-    int64_t batch = static_cast<int64_t>((size_t{2} << 30) / (px_bytes * P.samples));  // <= 2 GB of tiles
+    int64_t batch = static_cast<int64_t>((size_t{4} << 30) / (px_bytes * P.samples));  // <= 4 GB of tiles
     if (batch < 1) batch = 1;
     if (batch > rows) batch = rows;
     if (batch > 65535) batch = 65535;
@@ -490,6 +507,8 @@ hsad_status fullband_tc_launch(FbParams& P, cudaStream_t s, double* gram_out, do
         FbParams F = P;
         F.row_begin = rb;
         F.row_end = re;
+        // the kernel indexes its score map from its own row_begin
+        F.scores = static_cast<char*>(P.scores) + (rb - P.row_begin) * P.samples * static_cast<int64_t>(P.score_bytes);
         F.gram = gram;
         F.gram_row0 = rb;
         F.shift = su;

@@ -113,3 +113,17 @@ def test_pipeline_sharded_validates_on_host():
     e = _abi.PixelError()
     assert lib.hsad_pipeline_sharded(None, 4, 4, 8, 2, 4, req, 1, 0, C.byref(e)) == _abi.HSAD_E_INVALID_VALUE
     assert lib.hsad_last_error_message() == b"InvalidValue: n_strips must be >= 1"
+
+
+def test_fullband_gram_kernel_is_on_tcgen05():
+    """SASS evidence: the full-band Gram kernel issues UTCIMMA (tcgen05.mma kind::i8) with
+    TMEM loads, and no legacy mma.sync path stands in for it."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not on PATH")
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "tc_gram_kernel", str(_abi.LIB_PATH)],
+                          capture_output=True, text=True).stdout
+    if "UTCIMMA" not in sass:  # older cuobjdump: no substring match for -fun
+        sass = subprocess.run(["cuobjdump", "-sass", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "UTCIMMA" in sass and "LDTM" in sass
