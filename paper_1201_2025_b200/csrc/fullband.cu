@@ -418,12 +418,24 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
     FB_MARK(0);
 
     // this thread's tile of the lower triangle
+    // Tiles are dealt to threads column by column (tile column tk = threads
+    // [tk T - tk (tk - 1) / 2, ...) in row order): the tiles a Cholesky step has finished
+    // with are a prefix of the CTA, so whole warps drop out of the trailing update and the
+    // panel of a step sits in one warp (row-major dealing kept every warp issuing the 512-FMA
+    // update for a few live lanes until the last steps).
     const bool own = t < ntiles;
+    int tk = 0;
+#ifndef HSAD_FB_ROWMAJOR_TILES
+    while (tk + 1 < T && (tk + 1) * T - (tk + 1) * tk / 2 <= t) ++tk;
+    int ti = own ? tk + (t - (tk * T - tk * (tk - 1) / 2)) : 0;
+    if (!own) tk = 0;
+#else
     int ti = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
     while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
     while (ti * (ti + 1) / 2 > t) --ti;
-    const int tk = own ? t - ti * (ti + 1) / 2 : 0;
+    tk = own ? t - ti * (ti + 1) / 2 : 0;
     if (!own) ti = 0;
+#endif
     double acc[8][8];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -436,7 +448,7 @@ __global__ void __launch_bounds__(kFbRegThreads, 1) fullband_reg_kernel(const Fb
             // C = (N G - S S^T) / N^2 with G and S as exact (hi, lo) pairs: the difference is
             // formed in double-double arithmetic and rounded once, so a window whose mean is
             // far from the shift loses nothing to cancellation
-            const double2* g2 = reinterpret_cast<const double2*>(gpx + t * 128);
+            const double2* g2 = reinterpret_cast<const double2*>(gpx + (ti * (ti + 1) / 2 + tk) * 128);
             const double dN = N, invN2 = 1.0 / (dN * dN);
 #pragma unroll
             for (int a = 0; a < 8; ++a) {
