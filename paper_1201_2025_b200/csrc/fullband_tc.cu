@@ -487,6 +487,7 @@ hsad_status fullband_tc_launch(FbParams& P, cudaStream_t s, double* gram_out, do
     const size_t px_bytes = static_cast<size_t>(G.T) * (G.T + 1) / 2 * 128 * sizeof(double);  // (hi, lo) planes
     const int64_t rows = P.row_end - P.row_begin;
     int64_t batch = static_cast<int64_t>((size_t{4} << 30) / (px_bytes * P.samples));  // <= 4 GB of tiles
+    if (const int forced = env_int("HSAD_TC_BATCH_ROWS", 0); forced > 0) batch = forced;  // tests
     if (batch < 1) batch = 1;
     if (batch > rows) batch = rows;
     if (batch > 65535) batch = 65535;

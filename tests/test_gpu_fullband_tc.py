@@ -142,3 +142,16 @@ def test_tc_route_config_c3(orc, monkeypatch):
     assert e_k.max() <= max(e_o.max(), TOL64) * 1.05, (e_k.max(), e_o.max())
     assert (e_k > TOL64).sum() <= max((e_o > TOL64).sum(), 1) * 1.5
     assert np.median(e_k) < 1e-11
+
+
+def test_tc_route_row_batches_bit_identical(orc, monkeypatch):
+    """The Gram tiles are produced in row batches (<= 4 GB of tiles): forcing batches of 3 and
+    of 1 rows must reproduce the one-batch maps bit for bit (same digits, same walks)."""
+    monkeypatch.setenv("HSAD_FB_TC", "1")
+    cube = orc.port.random_cube(10, 57, 40, 5)
+    reqs = [hs.DetectRequest("lrx", W1(7)), hs.DetectRequest("dwrx", W2(3, 7))]
+    one = run(cube, reqs)
+    for rows in ("3", "1"):
+        monkeypatch.setenv("HSAD_TC_BATCH_ROWS", rows)
+        for x, y in zip(one, run(cube, reqs)):
+            assert np.array_equal(x, y)
