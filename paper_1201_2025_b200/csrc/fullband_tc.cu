@@ -19,8 +19,11 @@
 //      2W + 2E samples, one K = 32 chunk for the reference's LRX 15) instead of the whole
 //      window;
 //   4. after each step the tile is read back (tcgen05.ld), the 8 groups are recombined in
-//      int64 / fp64 (one rounding per entry) and written in the 8x8-tile order of
-//      fullband_reg_kernel, which subtracts the mean product and runs the Cholesky.
+//      int64 as hi * 2^28 + lo and stored as that exact (hi, lo) pair of doubles in the
+//      8x8-tile order of fullband_reg_kernel. Band L is a constant one, so row L of the Gram
+//      is the exact window sum S of every band; fullband_reg_kernel forms
+//      C = (N G - S S^T) / N^2 in double-double arithmetic (one rounding, no cancellation
+//      against the shift) and runs the Cholesky.
 // Operands are MN-major (band-contiguous, the cube's own BIP order), no swizzle: the digit
 // array in global memory is [sign][row][col][slice][192 bands] and a chunk is gathered with
 // 16-byte cp.async copies straight into the canonical UMMA layout.
@@ -50,7 +53,7 @@ constexpr int kTcSmem = kTcStages * kTcStage + 1024;   // > 114 KB: one CTA (512
 constexpr int kQBits = 54;                             // |q| < 2^54 (balanced 8 x 7-bit digits reach 0.496 * 2^56)
 
 struct TcParams {
-    const int8_t* q;        // digits: [2 signs][qrows][samples][8][192] + one zero sample
+    const int8_t* q;        // digits: [2 signs][qrows][samples][8][192] + one zero sample (address of padding copies)
     int64_t neg_off;        // byte offset of the negated copy
     int64_t zero_off;       // byte offset of the all-zero sample
     int lines, samples;
