@@ -184,3 +184,44 @@ def test_fp32_path_on_configs(orc, name, spec):
         top_g = set(np.argsort(-s.ravel(), kind="stable")[:k].tolist())
         top_o = set(np.argsort(-want.ravel(), kind="stable")[:k].tolist())
         assert top_g == top_o, f"{name} {a} top-{k}"
+
+
+def test_forked_groups_equal_sequential_groups(orc, monkeypatch):
+    """An asynchronous multi-group call runs groups 1.. on side streams forked from the
+    caller's stream and joined back into it: the maps must equal the sequential launch bit for
+    bit, and work queued on the caller's stream right after the call must see every map
+    (hsad_detect_multi and hsad_reduce_detect, on a non-default stream)."""
+    cube = torch.as_tensor(orc.port.random_cube(150, 260, 64, 11)).float().to(DEV)
+    W1, W2 = hs.WindowConfig.single, hs.WindowConfig.dual
+    reqs = []
+    for inner, outer in ((3, 7), (5, 11), (5, 15), (7, 21)):
+        reqs += [hs.DetectRequest("lrx", W1(outer)), hs.DetectRequest("dwrx", W2(inner, outer)),
+                 hs.DetectRequest("dwest", W2(inner, outer), eigcount=True)]
+    red = hs.reduce_cube(cube, 2, 4)
+    st = torch.full((1,), -1, dtype=torch.int64, device=DEV)
+
+    def sums(fn):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            outs = fn()
+            # consumers on the caller's stream, queued right behind the call
+            tot = [o[0].sum() for o in outs] + [o[1].double().sum() for o in outs if o[1] is not None]
+        side.synchronize()
+        return outs, [float(t) for t in tot]
+
+    monkeypatch.setenv("HSAD_NO_FORK", "1")
+    seq, seq_sums = sums(lambda: hs.detect_multi(red, reqs, status=st))
+    monkeypatch.delenv("HSAD_NO_FORK")
+    for _ in range(3):
+        frk, frk_sums = sums(lambda: hs.detect_multi(red, reqs, status=st))
+        assert frk_sums == seq_sums
+        for (a, ac), (b, bc) in zip(seq, frk):
+            assert torch.equal(a, b) and (ac is None or torch.equal(ac, bc))
+    assert int(st.item()) == -1
+    # hsad_reduce_detect: groups 1.. start right after the reduction, next to group 0
+    rf, fo = hs.reduce_detect(cube, reqs, 2, 4, status=st)
+    torch.cuda.synchronize()
+    assert torch.equal(rf, red)
+    for (a, ac), (b, bc) in zip(seq, fo):
+        assert torch.equal(a, b) and (ac is None or torch.equal(ac, bc))
