@@ -2116,7 +2116,10 @@ int64_t row_quantum(int64_t lines, int64_t samples) {
     const int64_t tw = HSAD_DET_NT * kcols_for(samples);
     const int64_t strips = (samples + tw - 1) / tw;
     // 32 measured best on C5 (24..128 sweep: within 1% of 24, 3.6% faster than 64)
-    int64_t q = 32;
+#ifndef HSAD_ROW_QUANTUM
+#define HSAD_ROW_QUANTUM 32
+#endif
+    int64_t q = HSAD_ROW_QUANTUM;
     while (q > 2 && strips * ((lines + q - 1) / q) < 2 * sms) q /= 2;
     return q;
 }
