@@ -27,6 +27,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -2152,15 +2153,25 @@ struct GroupFork {
     cudaStream_t side[kSide] = {};
     cudaEvent_t ready = nullptr, done[kSide] = {};
     bool ok = false;
+    GroupFork() = default;
+    GroupFork(const GroupFork&) = delete;
+    GroupFork& operator=(const GroupFork&) = delete;
+    ~GroupFork() {  // at thread exit (hsad_pipeline_sharded's workers); errors at process teardown are moot
+        for (int i = 0; i < kSide; ++i) {
+            if (side[i]) cudaStreamDestroy(side[i]);
+            if (done[i]) cudaEventDestroy(done[i]);
+        }
+        if (ready) cudaEventDestroy(ready);
+    }
 };
 GroupFork* group_fork() {
-    thread_local std::vector<GroupFork> ctx;
+    thread_local std::vector<std::unique_ptr<GroupFork>> ctx;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    for (GroupFork& g : ctx)
-        if (g.device == dev) return g.ok ? &g : nullptr;
-    ctx.emplace_back();
-    GroupFork& g = ctx.back();
+    for (auto& gp : ctx)
+        if (gp->device == dev) return gp->ok ? gp.get() : nullptr;
+    ctx.push_back(std::make_unique<GroupFork>());
+    GroupFork& g = *ctx.back();
     g.device = dev;
     bool ok = cudaEventCreateWithFlags(&g.ready, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < GroupFork::kSide && ok; ++i)
